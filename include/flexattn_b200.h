@@ -1,0 +1,251 @@
+/*
+ * flexattn_b200.h — C ABI of the B200-native FlexAttention hot path.
+ *
+ * This is the drop-in boundary for the reference's block-sparse attention
+ * library (`blockattn`, /root/reference/proj/include/blockattn/*.hpp). The
+ * reference has no FFI of its own: its boundary is the C++ API. Each entry
+ * point below replaces one reference function and cites it:
+ *
+ *   fa_create_block_mask   <- create_block_mask   block_mask.hpp:109-110 (+ transpose :115)
+ *   fa_transpose_block_mask<- transpose           block_mask.hpp:115, block_mask.cpp:161-178
+ *   fa_convert_block_mask  <- convert_block_mask  paged_kv.hpp:101, paged_kv.cpp:154-228
+ *   fa_flex_fwd            <- forward<Real>       engine.hpp:68-71, engine.cpp:46-172
+ *   fa_flex_bwd            <- backward<Real>      engine.hpp:78-82, engine.cpp:174-401
+ *   fa_flex_decode         <- decode<Real>        engine.hpp:92-96, engine.cpp:403-427
+ *                             (+ convert_mods     paged_kv.hpp:117, paged_kv.cpp:230-310
+ *                                when a page table is given)
+ *   fa_fill_uniform        <- random_tensor<Real> random.hpp:41-46 (SplitMix64 [-1,1))
+ *
+ * Conventions (all entry points):
+ *   - Caller-owned DEVICE buffers; plain pointers + sizes, no library types.
+ *   - Stream-ordered and asynchronous on the `stream` argument (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream). No internal host threads.
+ *   - No CPU fallback: a missing/unsupported GPU returns FA_CUDA_ERROR or
+ *     FA_UNSUPPORTED, never a silent host computation.
+ *   - Errors map 1:1 onto the reference exception classes (errors.hpp:11-101);
+ *     fa_last_error() returns the thread-local message of the last failure.
+ *   - Tensors are dense row-major (B, H, L, D) as reference Tensor4
+ *     (tensor.hpp:20-117). BlockMask indices are int32 (the reference uses
+ *     i64; values are identical, widening is exact).
+ */
+#ifndef FLEXATTN_B200_H_
+#define FLEXATTN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FA_API __attribute__((visibility("default")))
+#else
+#define FA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception class (errors.hpp) ------- */
+typedef int32_t fa_status;
+enum {
+  FA_OK = 0,
+  FA_SHAPE_MISMATCH = 1,          /* ShapeMismatch          errors.hpp:18 */
+  FA_NON_FINITE_INPUT = 2,        /* NonFiniteInput         errors.hpp:24 */
+  FA_INDEX_OUT_OF_RANGE = 3,      /* IndexOutOfRange        errors.hpp:30 */
+  FA_NON_POSITIVE_CAP = 4,        /* NonPositiveCap         errors.hpp:36 */
+  FA_GEOMETRY_MISMATCH = 5,       /* GeometryMismatch       errors.hpp:42 */
+  FA_BLOCK_MASK_MISMATCH = 6,     /* BlockMaskMismatch      errors.hpp:48 */
+  FA_STALE_STATISTICS = 7,        /* StaleStatistics        errors.hpp:55 */
+  FA_OFFSET_OUT_OF_RANGE = 8,     /* OffsetOutOfRange       errors.hpp:61 */
+  FA_OUT_OF_PAGES = 9,            /* OutOfPages             errors.hpp:67 */
+  FA_UNMAPPED_BLOCK = 10,         /* UnmappedBlock          errors.hpp:73 */
+  FA_UNMAPPED_PHYSICAL_INDEX = 11,/* UnmappedPhysicalIndex  errors.hpp:80 */
+  FA_CUDA_ERROR = 100,            /* CUDA runtime/driver failure            */
+  FA_UNSUPPORTED = 101            /* shape/dtype not compiled for sm_100a   */
+};
+
+/* ---- element types -------------------------------------------------------- */
+enum { FA_F32 = 0, FA_BF16 = 1 };
+
+/* ---- mask_mod descriptor ----------------------------------------------------
+ * A mask is the AND of the primitive terms whose bit is set in `terms`
+ * (and_mask, mask_library.cpp:94-98). An empty term set is noop_mask
+ * (mask_library.cpp:43-45). Every term sees q + q_offset (offset_mask,
+ * mask_library.cpp:106-110).
+ */
+enum {
+  FA_MASK_CAUSAL = 1u << 0,       /* q >= kv                        mask_library.cpp:13-15 */
+  FA_MASK_SLIDING_WINDOW = 1u << 1,/* q >= kv && q - kv <= window   mask_library.cpp:17-22 */
+  FA_MASK_DOCUMENT = 1u << 2,     /* ids[q] == ids[kv]              mask_library.cpp:24-34 */
+  FA_MASK_PREFIX_LM = 1u << 3,    /* kv < prefix || q >= kv         mask_library.cpp:36-41 */
+  FA_MASK_HASH = 1u << 4,         /* test aid hash_mask             tests/test_support.hpp:16-29 */
+  FA_MASK_NEVER = 1u << 5         /* test aid never_mask            tests/test_support.hpp:31-35 */
+};
+
+typedef struct fa_mask_desc {
+  uint32_t terms;          /* OR of FA_MASK_* bits; 0 = noop */
+  int32_t hash_density;    /* FA_MASK_HASH: true for density/256 of positions */
+  int64_t window;          /* FA_MASK_SLIDING_WINDOW (>= 0) */
+  int64_t prefix;          /* FA_MASK_PREFIX_LM (>= 0) */
+  int64_t q_offset;        /* offset_mask shift (decode); 0 otherwise */
+  uint64_t hash_seed;      /* FA_MASK_HASH */
+  const int32_t* doc_ids;  /* FA_MASK_DOCUMENT: device int32[doc_len] */
+  int64_t doc_len;
+} fa_mask_desc;
+
+/* ---- score_mod descriptor ---------------------------------------------------
+ * noop_score (mask_library.cpp:47-51) when `terms` == 0; FA_SCORE_ALIBI adds
+ * slopes[h]*(q-kv) (mask_library.cpp:53-69); FA_SCORE_SOFT_CAP applies
+ * cap*tanh(s/cap) (mask_library.cpp:83-92). Both set = compose(soft_cap, alibi)
+ * (modifiers.hpp:57-66): soft_cap(alibi(s)). Every term sees q + q_offset
+ * (offset_score, mask_library.cpp:112-119).
+ */
+enum { FA_SCORE_ALIBI = 1u << 0, FA_SCORE_SOFT_CAP = 1u << 1 };
+
+typedef struct fa_score_desc {
+  uint32_t terms;          /* OR of FA_SCORE_* bits; 0 = noop */
+  int32_t num_slopes;      /* length of slopes (indexed by q-head) */
+  double cap;              /* FA_SCORE_SOFT_CAP: finite, > 0 */
+  const float* slopes;     /* FA_SCORE_ALIBI: device float[num_slopes] */
+  int64_t q_offset;        /* offset_score shift (decode); 0 otherwise */
+} fa_score_desc;
+
+/* ---- BlockMask (device) -----------------------------------------------------
+ * Layout of reference BlockMask (block_mask.hpp:35-79) with the FlexAttention
+ * names: kv_num_blocks == partial_num, kv_indices == partial_idx,
+ * full_kv_* == full_*; q-side arrays == the same fields of transpose(bm).
+ * Counts (b_dims, h_dims, rows); indices (b_dims, h_dims, rows, cols);
+ * q-side counts (b_dims, h_dims, cols); q-side indices (b_dims, h_dims, cols, rows).
+ * Lists are ascending and compacted; slots past the count are 0
+ * (block_mask.cpp:50-52). The merged visit order of the reference is the
+ * ascending merge of the two lists (block_mask.hpp:26-31).
+ */
+typedef struct fa_block_mask {
+  int64_t b_dims, h_dims, rows, cols, bs_q, bs_kv, q_len, kv_len;
+  int32_t* kv_num_blocks;
+  int32_t* kv_indices;
+  int32_t* full_kv_num_blocks;
+  int32_t* full_kv_indices;
+  int32_t* q_num_blocks;       /* may be NULL when only the kv side is needed */
+  int32_t* q_indices;
+  int32_t* full_q_num_blocks;
+  int32_t* full_q_indices;
+} fa_block_mask;
+
+/* ---- dense (B, H, L, D) tensor view -------------------------------------- */
+typedef struct fa_tensor {
+  void* data;
+  int32_t dtype;           /* FA_F32 | FA_BF16 */
+  int32_t _pad;
+  int64_t b, h, l, d;
+} fa_tensor;
+
+/* ---- paged KV page table (device), reference PageTable paged_kv.hpp:18-41 --- */
+typedef struct fa_page_table {
+  int64_t batches, max_logical_pages, num_physical_pages, page_size;
+  const int32_t* table;            /* (batches, max_logical_pages), -1 = unmapped */
+  const int32_t* phys_to_logical;  /* (num_physical_pages), -1 = free */
+  const int32_t* owner;            /* (num_physical_pages), -1 = free */
+  const int32_t* seq_len;          /* (batches) tokens stored per sequence */
+} fa_page_table;
+
+/* ---- misc ------------------------------------------------------------------ */
+FA_API const char* fa_last_error(void);
+FA_API const char* fa_status_name(fa_status s);
+FA_API int32_t fa_abi_version(void);
+/* Number of kernel launches issued by this library since load (per process). */
+FA_API uint64_t fa_launch_count(void);
+
+/* ---- BlockMask ---------------------------------------------------------------
+ * Sizes the caller must allocate: rows/cols, element counts of each count and
+ * index array, and the scratch bytes create/transpose need.
+ */
+FA_API fa_status fa_block_mask_geometry(int64_t b_dims, int64_t h_dims, int64_t q_len, int64_t kv_len,
+                                 int64_t bs_q, int64_t bs_kv, int64_t* rows, int64_t* cols,
+                                 size_t* workspace_bytes);
+
+/* create_block_mask + transpose in one pass. `bm` holds the caller-allocated
+ * arrays; geometry fields are written. q-side arrays are filled when non-NULL. */
+FA_API fa_status fa_create_block_mask(const fa_mask_desc* mask, int64_t b_dims, int64_t h_dims,
+                               int64_t q_len, int64_t kv_len, int64_t bs_q, int64_t bs_kv,
+                               fa_block_mask* bm, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
+/* q-side arrays of `bm` from its kv-side arrays (transpose, block_mask.cpp:161-178). */
+FA_API fa_status fa_transpose_block_mask(fa_block_mask* bm, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+/* Rewrites every logical kv block index through the page table
+ * (convert_block_mask, paged_kv.cpp:154-228): out has b_dims = pt->batches,
+ * cols = num_physical_pages, kv_len = pages * page_size. `out` arrays are
+ * caller-allocated; q-side arrays of `out` are ignored. Unmapped blocks are
+ * reported with FA_UNMAPPED_BLOCK after the stream is synchronised by the call. */
+FA_API fa_status fa_convert_block_mask(const fa_block_mask* logical, const fa_page_table* pt,
+                                fa_block_mask* out, void* stream);
+
+/* ---- attention ---------------------------------------------------------------- */
+typedef struct fa_fwd_args {
+  fa_tensor q, k, v;       /* q (B,Hq,Q,D); k,v (B or 1, Hkv, KV, D) */
+  fa_tensor out;           /* (B,Hq,Q,D), dtype of q */
+  float* lse;              /* (B,Hq,Q) natural-log logsumexp; -inf on empty rows */
+  const fa_block_mask* bm; /* kv side required */
+  fa_mask_desc mask;
+  fa_score_desc score;
+  double scale;            /* <= 0 selects 1/sqrt(D) (config.hpp:28-31) */
+  int64_t gqa_group;       /* Hq == gqa_group * Hkv */
+} fa_fwd_args;
+
+typedef struct fa_bwd_args {
+  fa_tensor q, k, v, out, d_out;
+  const float* lse;        /* from fa_flex_fwd on the same tensors */
+  fa_tensor dq, dk, dv;    /* dq like q; dk/dv like k */
+  const fa_block_mask* bm; /* kv side and q side both required */
+  fa_mask_desc mask;
+  fa_score_desc score;
+  double scale;
+  int64_t gqa_group;
+  void* workspace;         /* fa_bwd_workspace_size bytes */
+  size_t workspace_bytes;
+} fa_bwd_args;
+
+typedef struct fa_decode_args {
+  fa_tensor q;             /* (B,Hq,n_new,D): rows [offset, offset+n_new) */
+  fa_tensor k_cache, v_cache; /* logical (B|1,Hkv,L,D) or physical (1,Hkv,pages*ps,D) */
+  fa_tensor out;
+  float* lse;
+  const fa_block_mask* bm; /* bm for the shifted mask at q_len == n_new (physical if pt) */
+  const fa_page_table* pt; /* NULL: unpaged; else logical positions recovered per page */
+  int64_t offset;
+  fa_mask_desc mask;       /* written in absolute positions (offset applied here) */
+  fa_score_desc score;
+  double scale;
+  int64_t gqa_group;
+  int32_t num_splits;      /* split-KV factor; <= 0 picks one */
+  int32_t _pad;
+  void* workspace;         /* fa_decode_workspace_size bytes */
+  size_t workspace_bytes;
+} fa_decode_args;
+
+FA_API fa_status fa_flex_fwd(const fa_fwd_args* args, void* stream);
+FA_API size_t fa_bwd_workspace_size(int64_t batch, int64_t heads, int64_t q_len, int64_t dim);
+FA_API fa_status fa_flex_bwd(const fa_bwd_args* args, void* stream);
+FA_API size_t fa_decode_workspace_size(int64_t batch, int64_t heads, int64_t n_new, int64_t dim,
+                                int32_t num_splits);
+FA_API fa_status fa_flex_decode(const fa_decode_args* args, void* stream);
+
+/* ---- synthetic inputs ------------------------------------------------------------
+ * Element i of random_tensor(seed, ...) (random.hpp:41-46):
+ * (float)(SplitMix64(seed) i-th draw in [-1,1)), rounded to bf16 (RNE) when dtype is bf16.
+ * Elements [first, first + n) are written to dst[0..n). */
+FA_API fa_status fa_fill_uniform(void* dst, int32_t dtype, uint64_t seed, int64_t first, int64_t n,
+                          void* stream);
+
+/* Scatter logical tokens (B, Hkv, L, D) into a physical paged buffer
+ * (1, Hkv, pages*ps, D) through `pt` (PagedKVCache::write_tokens, paged_kv.cpp:54-70). */
+FA_API fa_status fa_paged_write(const fa_tensor* logical, const fa_page_table* pt, fa_tensor* physical,
+                         void* stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* FLEXATTN_B200_H_ */

@@ -1,0 +1,774 @@
+"""Host-side mirror of the reference ``blockattn`` API over the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/blockattn/*.hpp so the parity tests read like the
+reference's own tests. Device memory, streams and dtypes come from PyTorch
+(plumbing only); every computation is one of this package's CUDA kernels,
+reached through ``libflexattn_b200.so``. There is no CPU path.
+
+    create_block_mask   block_mask.hpp:109-110   -> fa_create_block_mask
+    transpose           block_mask.hpp:115       -> (q-side arrays, fa_transpose_block_mask)
+    forward             engine.hpp:68-71         -> fa_flex_fwd
+    backward            engine.hpp:78-82         -> fa_flex_bwd
+    decode              engine.hpp:92-96         -> fa_flex_decode
+    PagedKVCache        paged_kv.hpp:50-89       (host page table; device K/V)
+    convert_block_mask  paged_kv.hpp:101         -> fa_convert_block_mask
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field, replace
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import (FA_BF16, FA_F32, BlockMaskC, BwdArgs, DecodeArgs, FwdArgs, MaskDesc,
+                   PageTableC, ScoreDesc, TensorC)
+
+# ---------------------------------------------------------------- errors (errors.hpp:11-101)
+
+
+class Error(RuntimeError):
+    """blockattn::Error."""
+
+
+class ShapeMismatch(Error): pass
+class NonFiniteInput(Error): pass
+class IndexOutOfRange(Error): pass
+class NonPositiveCap(Error): pass
+class GeometryMismatch(Error): pass
+class BlockMaskMismatch(Error): pass
+class StaleStatistics(Error): pass
+class OffsetOutOfRange(Error): pass
+class OutOfPages(Error): pass
+class UnmappedBlock(Error): pass
+class UnmappedPhysicalIndex(Error): pass
+class CudaError(Error): pass
+class Unsupported(Error): pass
+
+
+_STATUS = {1: ShapeMismatch, 2: NonFiniteInput, 3: IndexOutOfRange, 4: NonPositiveCap,
+           5: GeometryMismatch, 6: BlockMaskMismatch, 7: StaleStatistics, 8: OffsetOutOfRange,
+           9: OutOfPages, 10: UnmappedBlock, 11: UnmappedPhysicalIndex, 100: CudaError,
+           101: Unsupported}
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        lib = _lib.load()
+        msg = lib.fa_last_error().decode(errors="replace")
+        raise _STATUS.get(status, Error)(msg or lib.fa_status_name(status).decode())
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------- modifiers (mask_library.hpp)
+MASK_CAUSAL, MASK_SLIDING, MASK_DOCUMENT, MASK_PREFIX, MASK_HASH, MASK_NEVER = 1, 2, 4, 8, 16, 32
+SCORE_ALIBI, SCORE_SOFT_CAP = 1, 2
+
+
+@dataclass(frozen=True)
+class MaskMod:
+    """A mask_mod: AND of primitive terms (and_mask) with an optional q offset."""
+    terms: int = 0
+    window: int = 0
+    prefix: int = 0
+    q_offset: int = 0
+    hash_seed: int = 0
+    hash_density: int = 128
+    doc_ids: Optional[torch.Tensor] = field(default=None, compare=False)
+
+    def desc(self, device) -> MaskDesc:
+        d = MaskDesc()
+        d.terms, d.window, d.prefix, d.q_offset = self.terms, self.window, self.prefix, self.q_offset
+        d.hash_seed, d.hash_density = self.hash_seed, self.hash_density
+        if self.doc_ids is not None:
+            ids = _device_cache(self, "doc_ids", self.doc_ids, torch.int32, device)
+            d.doc_ids = ids.data_ptr()
+            d.doc_len = ids.numel()
+        return d
+
+
+@dataclass(frozen=True)
+class ScoreMod:
+    """A score_mod: soft_cap and/or alibi (composed as soft_cap(alibi(s)))."""
+    terms: int = 0
+    cap: float = 0.0
+    slopes: Optional[Sequence[float]] = field(default=None, compare=False)
+    q_offset: int = 0
+
+    @property
+    def identity(self) -> bool:
+        return self.terms == 0
+
+    def desc(self, device) -> ScoreDesc:
+        d = ScoreDesc()
+        d.terms, d.cap, d.q_offset = self.terms, float(self.cap), self.q_offset
+        if self.slopes is not None:
+            t = torch.as_tensor(list(self.slopes) if not torch.is_tensor(self.slopes) else self.slopes,
+                                dtype=torch.float32)
+            sl = _device_cache(self, "slopes", t, torch.float32, device)
+            d.slopes = sl.data_ptr()
+            d.num_slopes = sl.numel()
+        return d
+
+
+_CACHE: dict = {}
+
+
+def _device_cache(owner, name, t, dtype, device):
+    key = (id(owner), name, str(device))
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is owner:
+        return hit[1]
+    dev = torch.as_tensor(t).to(device=device, dtype=dtype).contiguous()
+    _CACHE[key] = (owner, dev)
+    return dev
+
+
+def noop_mask() -> MaskMod:
+    return MaskMod()
+
+
+def causal() -> MaskMod:
+    """q >= kv (mask_library.cpp:13-15)."""
+    return MaskMod(terms=MASK_CAUSAL)
+
+
+def sliding_window(window: int) -> MaskMod:
+    """q >= kv and q - kv <= window (mask_library.cpp:17-22)."""
+    if window < 0:
+        raise IndexOutOfRange(f"sliding_window: window must be >= 0, got {window}")
+    return MaskMod(terms=MASK_SLIDING, window=int(window))
+
+
+def document_mask(doc_ids) -> MaskMod:
+    """ids[q] == ids[kv] (mask_library.cpp:24-34)."""
+    return MaskMod(terms=MASK_DOCUMENT, doc_ids=torch.as_tensor(doc_ids).to(torch.int32))
+
+
+def prefix_lm(prefix_len: int) -> MaskMod:
+    """kv < prefix_len or q >= kv (mask_library.cpp:36-41)."""
+    if prefix_len < 0:
+        raise IndexOutOfRange(f"prefix_lm: prefix_len must be >= 0, got {prefix_len}")
+    return MaskMod(terms=MASK_PREFIX, prefix=int(prefix_len))
+
+
+def hash_mask(seed: int, density256: int = 128) -> MaskMod:
+    """Test aid of the reference (tests/test_support.hpp:16-29)."""
+    return MaskMod(terms=MASK_HASH, hash_seed=int(seed), hash_density=int(density256))
+
+
+def never_mask() -> MaskMod:
+    """Test aid of the reference (tests/test_support.hpp:31-35)."""
+    return MaskMod(terms=MASK_NEVER)
+
+
+def and_mask(a: MaskMod, b: MaskMod) -> MaskMod:
+    """and_mask (mask_library.cpp:94-98) for masks expressible as one term set."""
+    if a.q_offset != b.q_offset:
+        raise Unsupported("and_mask: operands with different offsets")
+    for attr in ("window", "prefix", "hash_seed"):
+        if getattr(a, attr) and getattr(b, attr) and getattr(a, attr) != getattr(b, attr):
+            raise Unsupported(f"and_mask: conflicting {attr}")
+    if a.doc_ids is not None and b.doc_ids is not None:
+        raise Unsupported("and_mask: two document masks")
+    hd = a.hash_density if a.terms & MASK_HASH else b.hash_density
+    return MaskMod(terms=a.terms | b.terms, window=a.window or b.window, prefix=a.prefix or b.prefix,
+                   q_offset=a.q_offset, hash_seed=a.hash_seed or b.hash_seed, hash_density=hd,
+                   doc_ids=a.doc_ids if a.doc_ids is not None else b.doc_ids)
+
+
+def offset_mask(m: MaskMod, offset: int) -> MaskMod:
+    """q -> q + offset (mask_library.cpp:106-110)."""
+    return replace(m, q_offset=m.q_offset + int(offset))
+
+
+def noop_score() -> ScoreMod:
+    return ScoreMod()
+
+
+def alibi_slopes(heads: int) -> list:
+    """-2^(-8(h+1)/H) (mask_library.cpp:71-81)."""
+    if heads < 1:
+        raise IndexOutOfRange(f"alibi_slopes: heads must be >= 1, got {heads}")
+    return [-(2.0 ** (-8.0 * (h + 1) / heads)) for h in range(heads)]
+
+
+def alibi(slopes) -> ScoreMod:
+    """s + slopes[h] * (q - kv) (mask_library.cpp:53-69)."""
+    return ScoreMod(terms=SCORE_ALIBI, slopes=list(map(float, slopes)))
+
+
+def soft_cap(cap: float) -> ScoreMod:
+    """cap * tanh(s / cap) (mask_library.cpp:83-92)."""
+    if not (cap > 0.0) or not math.isfinite(cap):
+        raise NonPositiveCap(f"soft_cap: cap must be finite and > 0, got {cap}")
+    return ScoreMod(terms=SCORE_SOFT_CAP, cap=float(cap))
+
+
+def compose(outer: ScoreMod, inner: ScoreMod) -> ScoreMod:
+    """outer(inner(s)) (modifiers.hpp:57-66); supported: soft_cap(alibi(s)) and identities."""
+    if outer.identity:
+        return inner
+    if inner.identity:
+        return outer
+    if outer.terms == SCORE_SOFT_CAP and inner.terms == SCORE_ALIBI and outer.q_offset == inner.q_offset:
+        return ScoreMod(terms=SCORE_ALIBI | SCORE_SOFT_CAP, cap=outer.cap, slopes=inner.slopes,
+                        q_offset=inner.q_offset)
+    raise Unsupported("compose: only soft_cap(alibi(s)) is compiled")
+
+
+def offset_score(s: ScoreMod, offset: int) -> ScoreMod:
+    """q -> q + offset (mask_library.cpp:112-119)."""
+    return replace(s, q_offset=s.q_offset + int(offset))
+
+
+# ---------------------------------------------------------------- config (config.hpp:16-45)
+@dataclass
+class AttentionConfig:
+    scale: Optional[float] = None
+    gqa_group: int = 1
+    block_size_q: int = 128
+    block_size_kv: int = 128
+
+    def effective_scale(self, head_dim: int) -> float:
+        return self.scale if self.scale is not None else 1.0 / math.sqrt(head_dim)
+
+    def validate(self):
+        if self.scale is not None and not (math.isfinite(self.scale) and self.scale > 0):
+            raise ShapeMismatch("AttentionConfig: scale must be finite and positive")
+        if self.gqa_group < 1:
+            raise ShapeMismatch(f"AttentionConfig: gqa_group must be >= 1, got {self.gqa_group}")
+        if self.block_size_q < 1 or self.block_size_kv < 1:
+            raise ShapeMismatch("AttentionConfig: block sizes must be >= 1")
+
+
+# ---------------------------------------------------------------- BlockMask (block_mask.hpp:35-79)
+@dataclass
+class BlockMask:
+    """Device BlockMask: FlexAttention names over the reference layout.
+
+    kv_num_blocks == partial_num, kv_indices == partial_idx, full_kv_* == full_*;
+    q_* arrays are the same fields of transpose(bm). int32 on the device.
+    ``mask`` is the runtime mask (the reference's runtime_mask minus bounds,
+    which the kernels apply from q_len/kv_len).
+    """
+    b_dims: int
+    h_dims: int
+    rows: int
+    cols: int
+    bs_q: int
+    bs_kv: int
+    q_len: int
+    kv_len: int
+    kv_num_blocks: torch.Tensor
+    kv_indices: torch.Tensor
+    full_kv_num_blocks: torch.Tensor
+    full_kv_indices: torch.Tensor
+    q_num_blocks: Optional[torch.Tensor] = None
+    q_indices: Optional[torch.Tensor] = None
+    full_q_num_blocks: Optional[torch.Tensor] = None
+    full_q_indices: Optional[torch.Tensor] = None
+    mask: Optional[MaskMod] = None
+
+    # reference-style accessors
+    @property
+    def partial_num(self): return self.kv_num_blocks
+    @property
+    def partial_idx(self): return self.kv_indices
+    @property
+    def full_num(self): return self.full_kv_num_blocks
+    @property
+    def full_idx(self): return self.full_kv_indices
+
+    def has_runtime_mask(self) -> bool:
+        return self.mask is not None
+
+    def c(self) -> BlockMaskC:
+        s = BlockMaskC()
+        s.b_dims, s.h_dims, s.rows, s.cols = self.b_dims, self.h_dims, self.rows, self.cols
+        s.bs_q, s.bs_kv, s.q_len, s.kv_len = self.bs_q, self.bs_kv, self.q_len, self.kv_len
+        for name in ("kv_num_blocks", "kv_indices", "full_kv_num_blocks", "full_kv_indices",
+                     "q_num_blocks", "q_indices", "full_q_num_blocks", "full_q_indices"):
+            t = getattr(self, name)
+            setattr(s, name, t.data_ptr() if t is not None else None)
+        return s
+
+    def with_mask(self, user_mask: MaskMod) -> "BlockMask":
+        return replace(self, mask=user_mask)
+
+    @property
+    def device(self):
+        return self.kv_num_blocks.device
+
+
+def _geometry(b_dims, h_dims, q_len, kv_len, bs_q, bs_kv):
+    lib = _lib.load()
+    rows, cols, ws = C.c_int64(), C.c_int64(), C.c_size_t()
+    _check(lib.fa_block_mask_geometry(b_dims, h_dims, q_len, kv_len, bs_q, bs_kv,
+                                      C.byref(rows), C.byref(cols), C.byref(ws)))
+    return rows.value, cols.value, ws.value
+
+
+def create_block_mask(mask: MaskMod, b_dims: int, h_dims: int, q_len: int, kv_len: int,
+                      bs_q: int = 128, bs_kv: int = 128, device="cuda", q_side: bool = True) -> BlockMask:
+    """create_block_mask (block_mask.cpp:79-115) + transpose, on the GPU."""
+    if mask is None:
+        raise ShapeMismatch("create_block_mask: mask has no callable")
+    rows, cols, ws = _geometry(b_dims, h_dims, q_len, kv_len, bs_q, bs_kv)
+    dev = torch.device(device)
+    i32 = dict(dtype=torch.int32, device=dev)
+    n = b_dims * h_dims
+    bm = BlockMask(b_dims, h_dims, rows, cols, bs_q, bs_kv, q_len, kv_len,
+                   torch.empty(n * rows, **i32), torch.empty(n * rows * cols, **i32),
+                   torch.empty(n * rows, **i32), torch.empty(n * rows * cols, **i32), mask=mask)
+    if q_side:
+        bm.q_num_blocks = torch.empty(n * cols, **i32)
+        bm.q_indices = torch.empty(n * cols * rows, **i32)
+        bm.full_q_num_blocks = torch.empty(n * cols, **i32)
+        bm.full_q_indices = torch.empty(n * cols * rows, **i32)
+    work = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+    cbm = bm.c()
+    md = mask.desc(dev)
+    with torch.cuda.device(dev):
+        _check(_lib.load().fa_create_block_mask(C.byref(md), b_dims, h_dims, q_len, kv_len, bs_q, bs_kv,
+                                                C.byref(cbm), C.c_void_p(work.data_ptr()), ws,
+                                                C.c_void_p(_stream())))
+    bm._work = work  # keep alive until the stream consumed it
+    return bm
+
+
+def transpose(bm: BlockMask) -> BlockMask:
+    """transpose (block_mask.cpp:161-178): q/kv roles swapped, same device arrays reused."""
+    if bm.q_num_blocks is None:
+        dev = bm.device
+        i32 = dict(dtype=torch.int32, device=dev)
+        n = bm.b_dims * bm.h_dims
+        bm.q_num_blocks = torch.empty(n * bm.cols, **i32)
+        bm.q_indices = torch.empty(n * bm.cols * bm.rows, **i32)
+        bm.full_q_num_blocks = torch.empty(n * bm.cols, **i32)
+        bm.full_q_indices = torch.empty(n * bm.cols * bm.rows, **i32)
+        ws = n * bm.rows * bm.cols
+        work = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+        cbm = bm.c()
+        _check(_lib.load().fa_transpose_block_mask(C.byref(cbm), C.c_void_p(work.data_ptr()), ws,
+                                                   C.c_void_p(_stream())))
+        bm._work_t = work
+    t = BlockMask(bm.b_dims, bm.h_dims, bm.cols, bm.rows, bm.bs_kv, bm.bs_q, bm.kv_len, bm.q_len,
+                  bm.q_num_blocks, bm.q_indices, bm.full_q_num_blocks, bm.full_q_indices,
+                  bm.kv_num_blocks, bm.kv_indices, bm.full_kv_num_blocks, bm.full_kv_indices,
+                  mask=None)
+    return t
+
+
+@dataclass
+class SparsityReport:
+    total_blocks: int
+    full_blocks: int
+    partial_blocks: int
+    empty_blocks: int
+    density: float
+
+
+def sparsity(bm: BlockMask) -> SparsityReport:
+    """sparsity (block_mask.cpp:180-191)."""
+    total = bm.b_dims * bm.h_dims * bm.rows * bm.cols
+    part = int(bm.kv_num_blocks.sum().item())
+    full = int(bm.full_kv_num_blocks.sum().item())
+    return SparsityReport(total, full, part, total - part - full,
+                          0.0 if total == 0 else (part + full) / total)
+
+
+# ---------------------------------------------------------------- tensors
+def _tensor(t: torch.Tensor, name: str) -> TensorC:
+    if t.dim() != 4:
+        raise ShapeMismatch(f"{name}: expected a (B, H, L, D) tensor, got {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise Unsupported(f"{name}: tensors must live on a CUDA device (no CPU path)")
+    if not t.is_contiguous():
+        raise ShapeMismatch(f"{name}: tensor must be contiguous")
+    if t.dtype == torch.bfloat16:
+        dt = FA_BF16
+    elif t.dtype == torch.float32:
+        dt = FA_F32
+    else:
+        raise Unsupported(f"{name}: dtype {t.dtype} (bf16 or fp32 only)")
+    s = TensorC()
+    s.data, s.dtype = t.data_ptr(), dt
+    s.b, s.h, s.l, s.d = t.shape
+    return s
+
+
+def _scale(cfg: AttentionConfig) -> float:
+    return float(cfg.scale) if cfg.scale is not None else 0.0
+
+
+@dataclass
+class AttentionOutput:
+    """engine.hpp:38-46: out (B,H,L,D) and lse (B,H,L) natural log."""
+    out: torch.Tensor
+    lse: torch.Tensor
+
+
+@dataclass
+class Gradients:
+    dq: torch.Tensor
+    dk: torch.Tensor
+    dv: torch.Tensor
+
+
+def _prep_mods(smod: ScoreMod, bm: BlockMask, mask: Optional[MaskMod]):
+    if smod is None:
+        raise BlockMaskMismatch("forward: score modifier has no callable")
+    m = mask if mask is not None else bm.mask
+    if m is None:
+        raise BlockMaskMismatch("forward: block mask has no runtime mask attached")
+    return m
+
+
+def forward(q, k, v, smod: ScoreMod, bm: BlockMask, cfg: Optional[AttentionConfig] = None,
+            mask: Optional[MaskMod] = None, out: Optional[torch.Tensor] = None,
+            lse: Optional[torch.Tensor] = None) -> AttentionOutput:
+    """forward<Real> (engine.cpp:46-172) on the GPU: bf16 -> tcgen05 kernel (bs 128,
+    D 64/128), otherwise the fp32 CUDA-core kernel."""
+    cfg = cfg or AttentionConfig()
+    cfg.validate()
+    m = _prep_mods(smod, bm, mask)
+    if bm.bs_q != cfg.block_size_q or bm.bs_kv != cfg.block_size_kv:
+        raise BlockMaskMismatch(f"block mask block sizes ({bm.bs_q},{bm.bs_kv}) disagree with config "
+                                f"({cfg.block_size_q},{cfg.block_size_kv})")
+    out = torch.empty_like(q) if out is None else out
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device) if lse is None else lse
+    a = FwdArgs()
+    a.q, a.k, a.v, a.out = _tensor(q, "q"), _tensor(k, "k"), _tensor(v, "v"), _tensor(out, "out")
+    a.lse = lse.data_ptr()
+    cbm = bm.c()
+    a.bm = C.pointer(cbm)
+    a.mask, a.score = m.desc(q.device), smod.desc(q.device)
+    a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
+    with torch.cuda.device(q.device):
+        _check(_lib.load().fa_flex_fwd(C.byref(a), C.c_void_p(_stream())))
+    return AttentionOutput(out, lse)
+
+
+def backward(q, k, v, fwd: AttentionOutput, d_out, smod: ScoreMod, bm: BlockMask,
+             bm_t: Optional[BlockMask] = None, cfg: Optional[AttentionConfig] = None,
+             mask: Optional[MaskMod] = None) -> Gradients:
+    """backward<Real> (engine.cpp:174-401): dQ/dK/dV through score_mod'. ``bm_t`` is
+    accepted for signature parity; the q-side arrays live in ``bm``."""
+    cfg = cfg or AttentionConfig()
+    cfg.validate()
+    m = _prep_mods(smod, bm, mask)
+    if bm.q_num_blocks is None:
+        transpose(bm)
+    if bm_t is not None and (bm_t.rows != bm.cols or bm_t.cols != bm.rows):
+        raise BlockMaskMismatch("backward: bm_t is not the transpose of bm")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    lib = _lib.load()
+    B, H, L, D = q.shape
+    ws = lib.fa_bwd_workspace_size(B, H, L, D)
+    work = _workspace(q.device, ws)
+    a = BwdArgs()
+    a.q, a.k, a.v = _tensor(q, "q"), _tensor(k, "k"), _tensor(v, "v")
+    a.out, a.d_out = _tensor(fwd.out, "out"), _tensor(d_out, "d_out")
+    if fwd.lse.numel() != B * H * L:
+        raise StaleStatistics("backward: saved forward statistics do not match these tensors")
+    a.lse = fwd.lse.data_ptr()
+    a.dq, a.dk, a.dv = _tensor(dq, "dq"), _tensor(dk, "dk"), _tensor(dv, "dv")
+    cbm = bm.c()
+    a.bm = C.pointer(cbm)
+    a.mask, a.score = m.desc(q.device), smod.desc(q.device)
+    a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
+    a.workspace, a.workspace_bytes = work.data_ptr(), ws
+    with torch.cuda.device(q.device):
+        _check(lib.fa_flex_bwd(C.byref(a), C.c_void_p(_stream())))
+    return Gradients(dq, dk, dv)
+
+
+_WS: dict = {}
+
+
+def _workspace(device, nbytes) -> torch.Tensor:
+    key = str(device)
+    w = _WS.get(key)
+    if w is None or w.numel() < nbytes:
+        w = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[key] = w
+    return w
+
+
+def decode(q_step, k_cache, v_cache, offset: int, mask: MaskMod, smod: ScoreMod, bm: BlockMask,
+           cfg: Optional[AttentionConfig] = None, page_table: Optional["PageTable"] = None,
+           num_splits: int = 0) -> AttentionOutput:
+    """decode (engine.cpp:403-427): q_step rows sit at [offset, offset+n_new). ``mask``/``smod``
+    speak absolute positions; ``bm`` describes the shifted mask at q_len = n_new (converted to
+    physical pages when ``page_table`` is given)."""
+    cfg = cfg or AttentionConfig()
+    cfg.validate()
+    if mask is None:
+        raise BlockMaskMismatch("decode: mask has no callable")
+    if smod is None:
+        raise BlockMaskMismatch("decode: score modifier has no callable")
+    out = torch.empty_like(q_step)
+    B, H, n_new, D = q_step.shape
+    lse = torch.empty((B, H, n_new), dtype=torch.float32, device=q_step.device)
+    lib = _lib.load()
+    ws = lib.fa_decode_workspace_size(B, H, n_new, D, num_splits)
+    work = _workspace(q_step.device, ws)
+    a = DecodeArgs()
+    a.q, a.k_cache, a.v_cache = _tensor(q_step, "q"), _tensor(k_cache, "k_cache"), _tensor(v_cache, "v_cache")
+    a.out = _tensor(out, "out")
+    a.lse = lse.data_ptr()
+    cbm = bm.c()
+    a.bm = C.pointer(cbm)
+    if page_table is not None:
+        cpt = page_table.c()
+        a.pt = C.pointer(cpt)
+    a.offset = int(offset)
+    a.mask, a.score = mask.desc(q_step.device), smod.desc(q_step.device)
+    a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
+    a.num_splits = int(num_splits)
+    a.workspace, a.workspace_bytes = work.data_ptr(), ws
+    with torch.cuda.device(q_step.device):
+        _check(lib.fa_flex_decode(C.byref(a), C.c_void_p(_stream())))
+    return AttentionOutput(out, lse)
+
+
+def flex_attention(query, key, value, score_mod: Optional[ScoreMod] = None,
+                   block_mask: Optional[BlockMask] = None, scale: Optional[float] = None,
+                   enable_gqa: bool = False, return_lse: bool = False):
+    """FlexAttention-style entry point (the north-star signature): forward over a BlockMask."""
+    if block_mask is None:
+        block_mask = create_block_mask(noop_mask(), 1, 1, query.shape[2], key.shape[2],
+                                       device=query.device)
+    g = query.shape[1] // key.shape[1]
+    if g != 1 and not enable_gqa:
+        raise ShapeMismatch("flex_attention: q/kv head counts differ; pass enable_gqa=True")
+    cfg = AttentionConfig(scale=scale, gqa_group=g, block_size_q=block_mask.bs_q,
+                          block_size_kv=block_mask.bs_kv)
+    res = forward(query, key, value, score_mod or noop_score(), block_mask, cfg)
+    return (res.out, res.lse) if return_lse else res.out
+
+
+# ---------------------------------------------------------------- synthetic inputs
+def random_tensor(seed: int, shape, dtype=torch.bfloat16, device="cuda", first: int = 0) -> torch.Tensor:
+    """random_tensor (random.hpp:41-46) generated on the device (bf16: RNE-rounded)."""
+    t = torch.empty(shape, dtype=dtype, device=device)
+    dt = FA_BF16 if dtype == torch.bfloat16 else FA_F32
+    with torch.cuda.device(t.device):
+        _check(_lib.load().fa_fill_uniform(C.c_void_p(t.data_ptr()), dt, C.c_uint64(seed & (2**64 - 1)),
+                                           first, t.numel(), C.c_void_p(_stream())))
+    return t
+
+
+# ---------------------------------------------------------------- paged KV (paged_kv.hpp)
+class _SplitMix64:
+    def __init__(self, seed):
+        self.s = seed & (2**64 - 1)
+
+    def next_u64(self):
+        self.s = (self.s + 0x9E3779B97F4A7C15) & (2**64 - 1)
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+        return z ^ (z >> 31)
+
+
+@dataclass
+class PageTable:
+    """PageTable (paged_kv.hpp:18-41), host copy plus device mirrors for the kernels."""
+    batches: int
+    max_logical_pages: int
+    num_physical_pages: int
+    page_size: int
+    table: list
+    phys_to_logical: list
+    owner: list
+    seq_len: list
+    _dev: dict = field(default_factory=dict, repr=False)
+
+    def lookup(self, b, logical_page):
+        return self.table[b * self.max_logical_pages + logical_page]
+
+    def device_arrays(self, device):
+        key = str(device)
+        if key not in self._dev:
+            i32 = dict(dtype=torch.int32, device=device)
+            self._dev[key] = (torch.tensor(self.table, **i32), torch.tensor(self.phys_to_logical, **i32),
+                              torch.tensor(self.owner, **i32), torch.tensor(self.seq_len, **i32))
+        return self._dev[key]
+
+    def c(self, device="cuda") -> PageTableC:
+        t, p2l, own, sl = self.device_arrays(torch.device(device))
+        s = PageTableC()
+        s.batches, s.max_logical_pages = self.batches, self.max_logical_pages
+        s.num_physical_pages, s.page_size = self.num_physical_pages, self.page_size
+        s.table, s.phys_to_logical, s.owner, s.seq_len = (t.data_ptr(), p2l.data_ptr(),
+                                                           own.data_ptr(), sl.data_ptr())
+        return s
+
+
+class PagedKVCache:
+    """PagedKVCache (paged_kv.hpp:50-89): LIFO free list (page 0 first), deterministic shuffle,
+    assign/append/erase with atomic capacity checks. K/V live on the device as
+    (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel."""
+
+    SENTINEL = -1
+
+    def __init__(self, batches, num_pages, page_size, kv_heads, dim, dtype=torch.bfloat16,
+                 device="cuda"):
+        if batches < 1 or num_pages < 1 or page_size < 1:
+            raise ShapeMismatch("PagedKVCache: batches, num_pages and page_size must be >= 1")
+        self.batches, self.num_pages, self.ps = batches, num_pages, page_size
+        self.kv_heads, self.dim = kv_heads, dim
+        self.device = torch.device(device)
+        self.k = torch.zeros((1, kv_heads, num_pages * page_size, dim), dtype=dtype, device=self.device)
+        self.v = torch.zeros_like(self.k)
+        self.table = [self.SENTINEL] * (batches * num_pages)
+        self.p2l = [self.SENTINEL] * num_pages
+        self.owner = [self.SENTINEL] * num_pages
+        self.seq = [0] * batches
+        self.free = [num_pages - 1 - p for p in range(num_pages)]  # LIFO: page 0 popped first
+
+    def page_table(self) -> PageTable:
+        return PageTable(self.batches, self.num_pages, self.num_pages, self.ps, list(self.table),
+                         list(self.p2l), list(self.owner), list(self.seq))
+
+    def shuffle_free_pages(self, seed: int):
+        """deterministic_shuffle (random.hpp:49-56)."""
+        rng = _SplitMix64(seed)
+        v = self.free
+        for i in range(len(v), 1, -1):
+            j = rng.next_u64() % i
+            v[i - 1], v[j] = v[j], v[i - 1]
+
+    def _check_batch(self, b):
+        if b < 0 or b >= self.batches:
+            raise IndexOutOfRange(f"PagedKVCache: batch {b} outside [0, {self.batches})")
+
+    def _take(self, b, lp):
+        page = self.free.pop()
+        self.table[b * self.num_pages + lp] = page
+        self.p2l[page] = lp
+        self.owner[page] = b
+
+    def erase(self, b):
+        self._check_batch(b)
+        owned = -(-self.seq[b] // self.ps)
+        for lp in range(owned):
+            slot = b * self.num_pages + lp
+            page = self.table[slot]
+            self.table[slot] = self.SENTINEL
+            self.p2l[page] = self.SENTINEL
+            self.owner[page] = self.SENTINEL
+            self.free.append(page)
+        self.seq[b] = 0
+
+    def assign(self, b, k_tokens, v_tokens):
+        """assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim) or (B', ...) slice."""
+        self._check_batch(b)
+        self._check_tokens(k_tokens, v_tokens)
+        n = k_tokens.shape[2]
+        needed = -(-n // self.ps)
+        owned = -(-self.seq[b] // self.ps)
+        if needed > len(self.free) + owned:
+            raise OutOfPages(f"PagedKVCache: assign of {n} tokens needs {needed} pages, only "
+                             f"{len(self.free) + owned} available")
+        self.erase(b)
+        for lp in range(needed):
+            self._take(b, lp)
+        self.seq[b] = n
+        self._write(b, 0, k_tokens, v_tokens)
+
+    def append_tokens(self, b, k_new, v_new):
+        """append_tokens (paged_kv.cpp:100-126)."""
+        self._check_batch(b)
+        self._check_tokens(k_new, v_new)
+        n = k_new.shape[2]
+        old = self.seq[b]
+        owned, total = -(-old // self.ps), -(-(old + n) // self.ps)
+        if total - owned > len(self.free):
+            raise OutOfPages(f"PagedKVCache: append of {n} tokens needs {total - owned} new pages, "
+                             f"only {len(self.free)} free")
+        for lp in range(owned, total):
+            self._take(b, lp)
+        self.seq[b] = old + n
+        self._write(b, old, k_new, v_new)
+
+    def _check_tokens(self, k_t, v_t):
+        if tuple(k_t.shape) != tuple(v_t.shape):
+            raise ShapeMismatch("PagedKVCache: k and v tokens must agree")
+        if k_t.shape[0] != 1 or k_t.shape[1] != self.kv_heads or k_t.shape[3] != self.dim:
+            raise ShapeMismatch(f"PagedKVCache: token tensors must be (1,{self.kv_heads},n,{self.dim})")
+
+    def _write(self, b, start, k_t, v_t):
+        # device scatter through a one-batch page table view (write_tokens, paged_kv.cpp:54-70)
+        n = k_t.shape[2]
+        if n == 0:
+            return
+        if start % self.ps != 0:
+            # unaligned append: shift tokens into a page-aligned staging buffer
+            pad = start % self.ps
+            ks = torch.zeros((1, self.kv_heads, pad + n, self.dim), dtype=self.k.dtype, device=self.device)
+            vs = torch.zeros_like(ks)
+            first_page = self.table[b * self.num_pages + start // self.ps]
+            base = first_page * self.ps
+            ks[:, :, :pad] = self.k[:, :, base:base + pad]
+            vs[:, :, :pad] = self.v[:, :, base:base + pad]
+            ks[:, :, pad:] = k_t
+            vs[:, :, pad:] = v_t
+            k_t, v_t, start = ks, vs, start - pad
+        lp0 = start // self.ps
+        npages = -(-k_t.shape[2] // self.ps)
+        row = self.table[b * self.num_pages + lp0: b * self.num_pages + lp0 + npages]
+        pt = PageTable(1, npages, self.num_pages, self.ps, row, self.p2l, self.owner, [k_t.shape[2]])
+        cpt = pt.c(self.device)
+        lib = _lib.load()
+        for src, dst in ((k_t, self.k), (v_t, self.v)):
+            src = src.to(device=self.device, dtype=self.k.dtype).contiguous()
+            s, d = _tensor(src, "tokens"), _tensor(dst, "cache")
+            with torch.cuda.device(self.device):
+                _check(lib.fa_paged_write(C.byref(s), C.byref(cpt), C.byref(d), C.c_void_p(_stream())))
+
+    def k_phys(self):
+        return self.k
+
+    def v_phys(self):
+        return self.v
+
+    def seq_len(self, b):
+        self._check_batch(b)
+        return self.seq[b]
+
+    def free_pages(self):
+        return len(self.free)
+
+    def max_tokens(self):
+        return self.num_pages * self.ps
+
+
+def convert_block_mask(bm: BlockMask, pt: PageTable) -> BlockMask:
+    """convert_block_mask (paged_kv.cpp:154-228) on the GPU: logical block columns -> pages."""
+    dev = bm.device
+    i32 = dict(dtype=torch.int32, device=dev)
+    rows, cols = bm.rows, pt.num_physical_pages
+    n = pt.batches * bm.h_dims
+    out = BlockMask(pt.batches, bm.h_dims, rows, cols, bm.bs_q, bm.bs_kv, bm.q_len,
+                    pt.num_physical_pages * pt.page_size, torch.empty(n * rows, **i32),
+                    torch.empty(n * rows * cols, **i32), torch.empty(n * rows, **i32),
+                    torch.empty(n * rows * cols, **i32), mask=bm.mask)
+    cl, co = bm.c(), out.c()
+    cpt = pt.c(dev)
+    _check(_lib.load().fa_convert_block_mask(C.byref(cl), C.byref(cpt), C.byref(co),
+                                             C.c_void_p(_stream())))
+    return out
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libflexattn_b200 in this process."""
+    return int(_lib.load().fa_launch_count())

@@ -1,0 +1,542 @@
+// fwd_sm100.cu — block-sparse FlexAttention forward for sm_100a (bf16 in,
+// fp32 accumulate), the tensor-core replacement of forward_impl
+// (engine.cpp:46-163).
+//
+// Persistent, warp-specialised CTA (320 threads, 1 CTA/SM). A work item is a
+// pair of 128-row query tiles (block rows 2p, 2p+1) of one (b, h):
+//   warps 0-3  softmax/correction/epilogue for tile 0   (thread = query row)
+//   warps 4-7  the same for tile 1
+//   warp  8    TMA producer: merges both rows' kv lists (partial + full,
+//              ascending = reference visit order) into a union list in smem,
+//              then streams Q (once) and K_j, V_j (per visited block) with
+//              cp.async.bulk.tensor into a 2-stage (D=128) ring. Empty blocks
+//              are never loaded.
+//   warp  9    MMA issuer (one thread): S_t = Q_t K_j^T (SS, TMEM fp32) and
+//              O_t += P_t V_j (TS: P from TMEM as bf16, V from smem, MN-major),
+//              ordered  QK0 QK1 | PV0(j) QK0(j+1) PV1(j) QK1(j+1) | ...  so the
+//              two tiles' softmax ping-pong against the tensor core.
+// TMEM (512 columns): S0 [0,128) S1 [128,256) (P_t aliases S_t's first 64
+// columns as packed bf16), O0 [256, 256+D), O1 [256+D, 256+2D).
+//
+// The softmax applies score_mod to every live score and mask_mod (with the
+// q<Q_LEN, kv<KV_LEN bounds of bound_mask, block_mask.cpp:14-19) only in
+// partial blocks; full blocks skip it. Rescaling of O is lazy: only when the
+// row max grows by more than 2^8 (exact math either way, since the final
+// normalisation uses the same stale max for O and l).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+#include "mods.cuh"
+#include "sm100_ptx.cuh"
+
+namespace fa {
+namespace {
+
+constexpr int kThreads = 320;  // 8 softmax warps + producer + MMA; <= 200 regs/thread
+constexpr int kTile = 128;           // query rows per tile == kv rows per block
+constexpr int kMaxCols = 1024;       // max kv blocks per row (KV_LEN <= 131072)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct FwdParams {
+  __nv_bfloat16* out;
+  float* lse;
+  int B, Hq, Hkv, Bkv, Lq, Lkv, G;
+  int bm_b, bm_h, rows, cols;
+  const int32_t* kv_num;
+  const int32_t* kv_idx;
+  const int32_t* full_num;
+  const int32_t* full_idx;
+  float scale, scale_log2;
+  int npairs, num_items;
+};
+
+template <int D>
+struct Cfg {
+  static constexpr int kChunks = D / 64;                  // 128-byte swizzle atoms along D
+  static constexpr int kStages = (D == 128) ? 2 : 4;      // K/V ring depth
+  static constexpr int kTileBytes = kTile * D * 2;        // one 128 x D bf16 tile
+  static constexpr int kChunkBytes = kTile * 128;         // 128 rows x 128 B
+};
+
+template <int D>
+struct alignas(1024) Smem {
+  uint8_t q[2][Cfg<D>::kTileBytes];
+  uint8_t k[Cfg<D>::kStages][Cfg<D>::kTileBytes];
+  uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
+  int32_t ulist[2][kMaxCols];
+  int32_t ulen[2];
+  uint64_t q_full[2], q_free[2];
+  uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages], kv_empty[Cfg<D>::kStages];
+  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t item_full[2], item_empty[2];
+  uint32_t tmem_base;
+};
+
+// union-list entry: block column | tile-membership and full-block flags
+constexpr uint32_t kIn0 = 1u << 24, kFull0 = 1u << 25, kIn1 = 1u << 26, kFull1 = 1u << 27;
+constexpr uint32_t kColMask = (1u << 24) - 1;
+
+struct Item {
+  int b, h, pair;
+};
+__device__ __forceinline__ Item decode_item(const FwdParams& p, int item) {
+  // heaviest (highest) row pairs first across all heads: a cheap LPT order for causal-like masks
+  const int bh_count = p.B * p.Hq;
+  const int pr = p.npairs - 1 - item / bh_count;
+  const int bh = item % bh_count;
+  return Item{bh / p.Hq, bh % p.Hq, pr};
+}
+
+template <int D, class MaskT, class ScoreT>
+__global__ void __launch_bounds__(kThreads, 1)
+    flex_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const FwdParams p, MaskT mask,
+                          ScoreT score) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem<D>& sm = *reinterpret_cast<Smem<D>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm.q_full[t], 1);
+      mbar_init(&sm.q_free[t], 1);
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.o_full[t], 1);
+      mbar_init(&sm.item_full[t], 1);
+      mbar_init(&sm.item_empty[t], 1 + 8);
+    }
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 8 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  if (warp == 9) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp >= 8) {
+    if (warp == 8 && lane == 0) {
+      // ===================== TMA producer =====================
+      int kv_it = 0;
+      int n = 0;
+      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
+        const Item it = decode_item(p, item);
+        const int buf = n & 1;
+        mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
+        // ---- union of the two rows' visit lists (ascending merge) ----
+        const int mb = p.bm_b == 1 ? 0 : it.b, mh = p.bm_h == 1 ? 0 : it.h;
+        const int r0 = 2 * it.pair, r1 = r0 + 1;
+        const long long s0 = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r0;
+        const int np0 = __ldg(p.kv_num + s0), nf0 = __ldg(p.full_num + s0);
+        const int np1 = r1 < p.rows ? __ldg(p.kv_num + s0 + 1) : 0;
+        const int nf1 = r1 < p.rows ? __ldg(p.full_num + s0 + 1) : 0;
+        const int32_t* pi0 = p.kv_idx + s0 * p.cols;
+        const int32_t* fi0 = p.full_idx + s0 * p.cols;
+        const int32_t* pi1 = pi0 + p.cols;
+        const int32_t* fi1 = fi0 + p.cols;
+        int a = 0, bq = 0, c = 0, d = 0, len = 0;
+        int va = a < np0 ? __ldg(pi0 + a) : 0x7fffffff;
+        int vb = bq < nf0 ? __ldg(fi0 + bq) : 0x7fffffff;
+        int vc = c < np1 ? __ldg(pi1 + c) : 0x7fffffff;
+        int vd = d < nf1 ? __ldg(fi1 + d) : 0x7fffffff;
+        while (true) {
+          const int col = min(min(va, vb), min(vc, vd));
+          if (col == 0x7fffffff) break;
+          uint32_t e = static_cast<uint32_t>(col);
+          if (va == col) { e |= kIn0; ++a; va = a < np0 ? __ldg(pi0 + a) : 0x7fffffff; }
+          if (vb == col) { e |= kIn0 | kFull0; ++bq; vb = bq < nf0 ? __ldg(fi0 + bq) : 0x7fffffff; }
+          if (vc == col) { e |= kIn1; ++c; vc = c < np1 ? __ldg(pi1 + c) : 0x7fffffff; }
+          if (vd == col) { e |= kIn1 | kFull1; ++d; vd = d < nf1 ? __ldg(fi1 + d) : 0x7fffffff; }
+          sm.ulist[buf][len++] = static_cast<int32_t>(e);
+        }
+        sm.ulen[buf] = len;
+        mbar_arrive(&sm.item_full[buf]);
+        // ---- Q tiles ----
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&sm.q_free[t], (n & 1) ^ 1);
+          mbar_expect_tx(&sm.q_full[t], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.q[t] + ch * C::kChunkBytes, &tmQ, &sm.q_full[t], ch * 64,
+                        (r0 + t) * kTile, it.b * p.Hq + it.h);
+        }
+        // ---- K/V blocks ----
+        const int kb = p.Bkv == 1 ? 0 : it.b, kh = it.h / p.G;
+        for (int j = 0; j < len; ++j, ++kv_it) {
+          const int st = kv_it % C::kStages;
+          mbar_wait(&sm.kv_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          const int colb = static_cast<int>(static_cast<uint32_t>(sm.ulist[buf][j]) & kColMask);
+          mbar_expect_tx(&sm.k_full[st], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.k[st] + ch * C::kChunkBytes, &tmK, &sm.k_full[st], ch * 64,
+                        colb * kTile, kb * p.Hkv + kh);
+          mbar_expect_tx(&sm.v_full[st], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.v[st] + ch * C::kChunkBytes, &tmV, &sm.v_full[st], ch * 64,
+                        colb * kTile, kb * p.Hkv + kh);
+        }
+      }
+    } else if (warp == 9 && lane == 0) {
+      // ===================== MMA issuer =====================
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
+      uint32_t p_phase[2] = {0, 0};
+      int kv_it = 0;
+      int n = 0;
+      auto issue_qk = [&](int t, int st) {
+        const uint32_t kaddr = smem_u32(sm.k[st]);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kChunkBytes + (kk & 3) * 32;
+          const uint64_t ad = make_sdesc_sw128(q_addr[t] + off, 16, 1024);
+          const uint64_t bd = make_sdesc_sw128(kaddr + off, 16, 1024);
+          umma_ss(tmem + t * 128, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm.s_full[t]);
+      };
+      auto issue_pv = [&](int t, int st, bool acc) {
+        const uint32_t vaddr = smem_u32(sm.v[st]);
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          const uint64_t bd = make_sdesc_sw128(vaddr + kk * 2048, C::kChunkBytes, 1024);
+          umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, bd, idesc_pv,
+                  (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
+        const int buf = n & 1;
+        mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+        const int len = sm.ulen[buf];
+        const uint32_t* U = reinterpret_cast<const uint32_t*>(sm.ulist[buf]);
+        mbar_wait(&sm.q_full[0], n & 1);
+        mbar_wait(&sm.q_full[1], n & 1);
+        tc_fence_after();
+        bool first_pv[2] = {true, true};
+        if (len > 0) {
+          const int st0 = kv_it % C::kStages;
+          mbar_wait(&sm.k_full[st0], (kv_it / C::kStages) & 1);
+          tc_fence_after();
+          const uint32_t e0 = U[0];
+          if (e0 & kIn0) issue_qk(0, st0);
+          if (e0 & kIn1) issue_qk(1, st0);
+        }
+        for (int j = 0; j < len; ++j) {
+          const int it_j = kv_it + j;
+          const int st = it_j % C::kStages;
+          const uint32_t e = U[j];
+          const uint32_t en = (j + 1 < len) ? U[j + 1] : 0u;
+          const int st1 = (it_j + 1) % C::kStages;
+          bool k1_ready = false;
+          mbar_wait(&sm.v_full[st], (it_j / C::kStages) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t in_bit = t == 0 ? kIn0 : kIn1;
+            if (e & in_bit) {
+              mbar_wait(&sm.p_full[t], p_phase[t]);
+              p_phase[t] ^= 1;
+              tc_fence_after();
+              issue_pv(t, st, !first_pv[t]);
+              first_pv[t] = false;
+            }
+            if (en & in_bit) {
+              if (!k1_ready) {
+                mbar_wait(&sm.k_full[st1], ((it_j + 1) / C::kStages) & 1);
+                tc_fence_after();
+                k1_ready = true;
+              }
+              issue_qk(t, st1);
+            }
+          }
+          umma_commit(&sm.kv_empty[st]);
+        }
+        kv_it += len;
+        for (int t = 0; t < 2; ++t) {
+          umma_commit(&sm.o_full[t]);
+          umma_commit(&sm.q_free[t]);
+        }
+        mbar_arrive(&sm.item_empty[buf]);
+      }
+    }
+  } else {
+    // ===================== softmax / correction / epilogue =====================
+    const int t = warp >> 2;               // tile
+    const int wq = warp & 3;               // TMEM lane quarter
+    const int row = wq * 32 + lane;        // query row within the tile
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t s_tm = tmem + lane_base + t * 128;
+    const uint32_t o_tm = tmem + lane_base + 256 + t * D;
+    const uint32_t in_bit = t == 0 ? kIn0 : kIn1;
+    const uint32_t full_bit = t == 0 ? kFull0 : kFull1;
+    uint32_t s_phase = 0;
+    int n = 0;
+    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
+      const Item it = decode_item(p, item);
+      const int buf = n & 1;
+      mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+      const int len = sm.ulen[buf];
+      const int qi = (2 * it.pair + t) * kTile + row;
+      float m = -INFINITY, l = 0.f;
+      bool any_blocks = false;
+      for (int j = 0; j < len; ++j) {
+        const uint32_t e = static_cast<uint32_t>(sm.ulist[buf][j]);
+        if (!(e & in_bit)) continue;
+        any_blocks = true;
+        const bool full = (e & full_bit) != 0;
+        const int kv0 = static_cast<int>(e & kColMask) * kTile;
+        mbar_wait(&sm.s_full[t], s_phase);
+        s_phase ^= 1;
+        tc_fence_after();
+        // pass 1: score_mod (+ mask_mod and bounds in partial blocks), row max.
+        // Modified scores are written back to TMEM unless they are a plain scale.
+        constexpr bool kPlain = ScoreT::kIdentity;
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          const int kvc = kv0 + cc * 32;
+          uint32_t bits = 0xffffffffu;
+          if (!full) {
+            bits = 0;
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              const int kv = kvc + i;
+              const bool ok = qi < p.Lq && kv < p.Lkv && mask(it.b, it.h, qi, kv);
+              bits |= static_cast<uint32_t>(ok) << i;
+            }
+          }
+          uint32_t r[32];
+          tmem_ld32(s_tm + cc * 32, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float v;
+            if constexpr (kPlain) {
+              v = __uint_as_float(r[i]) * p.scale_log2;
+            } else {
+              v = score.apply(__uint_as_float(r[i]) * p.scale, it.b, it.h, qi, kvc + i) * kLog2e;
+            }
+            v = ((bits >> i) & 1u) ? v : -INFINITY;
+            r[i] = __float_as_uint(v);
+            mx = fmaxf(mx, v);
+          }
+          if (!kPlain || !full) tmem_st32(s_tm + cc * 32, r);
+        }
+        if (!kPlain || !full) tmem_wait_st();
+        // lazy rescale (warp-uniform decision; tcgen05.ld/st are warp-collective)
+        const float m_new = fmaxf(m, mx);
+        const bool need = (m != -INFINITY) && (m_new > m + kRescaleThreshold);
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? ex2(m - m_new) : 1.f;
+#pragma unroll 1
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t r[32];
+            tmem_ld32(o_tm + cc * 32, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(o_tm + cc * 32, r);
+          }
+          l *= alpha;
+        }
+        if (need || m == -INFINITY) m = m_new;
+        const float msub = (m == -INFINITY) ? 0.f : m;
+        // pass 2: P = exp2(x - m) as packed bf16 into S's first 64 columns (64 scores per step)
+        const float xs = (kPlain && full) ? p.scale_log2 : 1.f;
+        float lsum = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t a[32], b2[32], r[32];
+          tmem_ld32(s_tm + cc * 64, a);
+          tmem_ld32(s_tm + cc * 64 + 32, b2);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ex2(fmaf(__uint_as_float(a[2 * i]), xs, -msub));
+            const float p1 = ex2(fmaf(__uint_as_float(a[2 * i + 1]), xs, -msub));
+            const float p2 = ex2(fmaf(__uint_as_float(b2[2 * i]), xs, -msub));
+            const float p3 = ex2(fmaf(__uint_as_float(b2[2 * i + 1]), xs, -msub));
+            lsum += (p0 + p1) + (p2 + p3);
+            r[i] = pack_bf16(p0, p1);
+            r[16 + i] = pack_bf16(p2, p3);
+          }
+          tmem_st32(s_tm + cc * 32, r);
+        }
+        l += lsum;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
+      }
+      // ---- epilogue: O / l -> bf16, lse ----
+      mbar_wait(&sm.o_full[t], n & 1);
+      tc_fence_after();
+      const bool valid = qi < p.Lq;
+      const long long slot = (static_cast<long long>(it.b) * p.Hq + it.h) * p.Lq + qi;
+      __nv_bfloat16* orow = p.out + slot * D;
+      if (any_blocks) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(o_tm + cc * 32, r);
+          tmem_wait_ld();
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(r[v4 * 8 + 0]) * inv, __uint_as_float(r[v4 * 8 + 1]) * inv);
+              w.y = pack_bf16(__uint_as_float(r[v4 * 8 + 2]) * inv, __uint_as_float(r[v4 * 8 + 3]) * inv);
+              w.z = pack_bf16(__uint_as_float(r[v4 * 8 + 4]) * inv, __uint_as_float(r[v4 * 8 + 5]) * inv);
+              w.w = pack_bf16(__uint_as_float(r[v4 * 8 + 6]) * inv, __uint_as_float(r[v4 * 8 + 7]) * inv);
+              dst[v4] = w;
+            }
+          }
+        }
+      } else if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow);
+        for (int v4 = 0; v4 < D / 8; ++v4) dst[v4] = make_uint4(0, 0, 0, 0);
+      }
+      if (valid) p.lse[slot] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// 3-D map over a (BH, L, D) bf16 tensor, box (64, 128, 1), 128-byte swizzle.
+fa_status make_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
+  EncodeTiledFn enc = get_encode();
+  FA_REQUIRE(enc != nullptr, FA_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(len),
+                        static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2,
+                           static_cast<cuuint64_t>(len) * d * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  FA_REQUIRE(r == CUDA_SUCCESS, FA_CUDA_ERROR,
+             "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return FA_OK;
+}
+
+template <int D, class MaskT, class ScoreT>
+fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
+              const BmView& bm, MaskT mask, ScoreT score, cudaStream_t st) {
+  CUtensorMap mq, mk, mv;
+  fa_status s;
+  if ((s = make_map(&mq, q, g.B * g.Hq, g.Lq, D)) != FA_OK) return s;
+  if ((s = make_map(&mk, k, g.Bkv * g.Hkv, g.Lkv, D)) != FA_OK) return s;
+  if ((s = make_map(&mv, v, g.Bkv * g.Hkv, g.Lkv, D)) != FA_OK) return s;
+  FwdParams p{};
+  p.out = static_cast<__nv_bfloat16*>(o);
+  p.lse = lse;
+  p.B = g.B; p.Hq = g.Hq; p.Hkv = g.Hkv; p.Bkv = g.Bkv; p.Lq = g.Lq; p.Lkv = g.Lkv; p.G = g.G;
+  p.bm_b = g.bm_b; p.bm_h = g.bm_h; p.rows = g.rows; p.cols = g.cols;
+  p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.full_num = bm.full_num; p.full_idx = bm.full_idx;
+  p.scale = g.scale;
+  p.scale_log2 = g.scale * kLog2e;
+  p.npairs = (g.rows + 1) / 2;
+  p.num_items = g.B * g.Hq * p.npairs;
+  const size_t smem = sizeof(Smem<D>) + 1024;
+  auto kern = flex_fwd_sm100_kernel<D, MaskT, ScoreT>;
+  FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
+  if (grid <= 0) return FA_OK;
+  kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, p, mask, score);
+  count_launch();
+  FA_CHECK_CUDA(cudaGetLastError());
+  return FA_OK;
+}
+
+template <int D, class ScoreT>
+fa_status by_mask(const AttnGeom& g, const void* q, const void* k, const void* v, void* o,
+                  float* lse, const BmView& bm, const MaskParams& mp, int mk, ScoreT s,
+                  cudaStream_t st) {
+  switch (mk) {
+    case kMaskNoop: return run<D>(g, q, k, v, o, lse, bm, MaskFn<kMaskNoop>{mp}, s, st);
+    case kMaskCausalOnly: return run<D>(g, q, k, v, o, lse, bm, MaskFn<kMaskCausalOnly>{mp}, s, st);
+    case kMaskSlidingOnly: return run<D>(g, q, k, v, o, lse, bm, MaskFn<kMaskSlidingOnly>{mp}, s, st);
+    case kMaskDocCausal: return run<D>(g, q, k, v, o, lse, bm, MaskFn<kMaskDocCausal>{mp}, s, st);
+    default: return run<D>(g, q, k, v, o, lse, bm, MaskFn<kMaskDynamic>{mp}, s, st);
+  }
+}
+
+template <int D>
+fa_status by_score(const AttnGeom& g, const void* q, const void* k, const void* v, void* o,
+                   float* lse, const BmView& bm, const MaskParams& mp, int mk,
+                   const ScoreParams& sp, int sk, cudaStream_t st) {
+  switch (sk) {
+    case 0: return by_mask<D>(g, q, k, v, o, lse, bm, mp, mk, ScoreFn<0>{sp}, st);
+    case 1: return by_mask<D>(g, q, k, v, o, lse, bm, mp, mk, ScoreFn<1>{sp}, st);
+    case 2: return by_mask<D>(g, q, k, v, o, lse, bm, mp, mk, ScoreFn<2>{sp}, st);
+    default: return by_mask<D>(g, q, k, v, o, lse, bm, mp, mk, ScoreFn<3>{sp}, st);
+  }
+}
+
+}  // namespace
+
+bool fwd_sm100_supported(const AttnGeom& g) {
+  return (g.D == 128 || g.D == 64) && g.bs_q == kTile && g.bs_kv == kTile && g.cols <= kMaxCols;
+}
+
+fa_status launch_fwd_sm100(const AttnGeom& g, const void* q, const void* k, const void* v, void* o,
+                           float* lse, const BmView& bm, const MaskParams& mp, int mkind,
+                           const ScoreParams& sp, int skind, cudaStream_t st) {
+  if (g.D == 128) return by_score<128>(g, q, k, v, o, lse, bm, mp, mkind, sp, skind, st);
+  return by_score<64>(g, q, k, v, o, lse, bm, mp, mkind, sp, skind, st);
+}
+
+}  // namespace fa

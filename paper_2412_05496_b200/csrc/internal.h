@@ -1,0 +1,88 @@
+// internal.h — host-side plumbing shared by the C-ABI translation units:
+// thread-local error state, status helpers, launch accounting and the
+// internal launcher signatures (templates cannot cross the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/flexattn_b200.h"
+#include "mods.cuh"
+
+namespace fa {
+
+fa_status set_error(fa_status s, const std::string& msg);
+void clear_error();
+fa_status cuda_status(cudaError_t e, const char* what);
+void count_launch(uint64_t n = 1);
+int num_sms();
+
+#define FA_CHECK_CUDA(expr)                                          \
+  do {                                                               \
+    cudaError_t e__ = (expr);                                        \
+    if (e__ != cudaSuccess) return ::fa::cuda_status(e__, #expr);    \
+  } while (0)
+
+#define FA_REQUIRE(cond, status, msg)                                \
+  do {                                                               \
+    if (!(cond)) return ::fa::set_error((status), (msg));            \
+  } while (0)
+
+// Host mirror of the descriptors (validated, device pointers).
+MaskParams to_mask_params(const fa_mask_desc& d);
+ScoreParams to_score_params(const fa_score_desc& d);
+// Pick the specialised kernel kind for a term set (kMaskDynamic if none matches).
+int mask_kind_of(uint32_t terms);
+
+// Geometry of the forward problem, shared by the launchers.
+struct AttnGeom {
+  int B, Hq, Hkv, Bkv, Lq, Lkv, D, G;
+  int bm_b, bm_h, rows, cols, bs_q, bs_kv;
+  float scale;
+};
+
+struct BmView {
+  const int32_t* kv_num;
+  const int32_t* kv_idx;
+  const int32_t* full_num;
+  const int32_t* full_idx;
+};
+
+fa_status launch_fwd_simt(const AttnGeom& g, const void* q, const void* k, const void* v, void* o,
+                          float* lse, int dtype, const BmView& bm, const MaskParams& mp,
+                          int mkind, const ScoreParams& sp, int skind, cudaStream_t st);
+
+bool fwd_sm100_supported(const AttnGeom& g);
+fa_status launch_fwd_sm100(const AttnGeom& g, const void* q, const void* k, const void* v, void* o,
+                           float* lse, const BmView& bm, const MaskParams& mp, int mkind,
+                           const ScoreParams& sp, int skind, cudaStream_t st);
+
+struct DecodeGeom {
+  AttnGeom a;        // Lq = n_new, Lkv = cache length (physical when paged)
+  int num_splits;
+  int logical_kv;    // kv bound in logical coordinates (cache length / seq_len source)
+};
+struct PageView {
+  const int32_t* phys_to_logical;
+  const int32_t* owner;
+  const int32_t* seq_len;
+  int page_size;
+  int enabled;
+};
+
+fa_status launch_decode(const DecodeGeom& g, const void* q, const void* k, const void* v, void* o,
+                        float* lse, const BmView& bm, const PageView& pv, const MaskParams& mp,
+                        int mkind, const ScoreParams& sp, int skind, void* workspace,
+                        cudaStream_t st);
+
+bool bwd_sm100_supported(const AttnGeom& g);
+fa_status launch_bwd(const AttnGeom& g, const void* q, const void* k, const void* v,
+                     const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                     void* dv, int dtype, const BmView& bm, const BmView& bmt,
+                     const MaskParams& mp, int mkind, const ScoreParams& sp, int skind,
+                     void* workspace, cudaStream_t st);
+
+}  // namespace fa

@@ -1,0 +1,129 @@
+// mods.cuh — mask_mod / score_mod as device functors inlined into the
+// templated kernels (the reference's std::function callables,
+// modifiers.hpp:17-40, evaluated in double; here fp32 on device).
+//
+// A mask functor is any type with
+//     __device__ bool operator()(int b, int h, int q, int kv) const;
+// A score functor is any type with
+//     static constexpr bool kIdentity;
+//     __device__ float apply(float s, int b, int h, int q, int kv) const;  // s = scaled score
+//     __device__ float grad (float s, int b, int h, int q, int kv) const;  // d apply / d s
+// The built-in ones below cover the reference mask library
+// (mask_library.cpp) and are what the C ABI dispatches to.
+#pragma once
+
+#include <stdint.h>
+
+#include "sm100_ptx.cuh"
+
+namespace fa {
+
+struct MaskParams {
+  uint32_t terms;
+  int32_t hash_density;
+  int32_t window;
+  int32_t prefix;
+  int32_t q_offset;
+  int32_t doc_len;
+  uint64_t hash_seed;
+  const int32_t* doc_ids;
+};
+
+struct ScoreParams {
+  uint32_t terms;
+  int32_t q_offset;
+  float cap;
+  float inv_cap;
+  const float* slopes;
+};
+
+enum : uint32_t {
+  kMaskCausal = 1u << 0,
+  kMaskSliding = 1u << 1,
+  kMaskDocument = 1u << 2,
+  kMaskPrefix = 1u << 3,
+  kMaskHash = 1u << 4,
+  kMaskNever = 1u << 5,
+};
+
+// Specialised mask kinds the kernels are instantiated for; kMaskDynamic
+// evaluates any AND-combination of terms from the runtime bit set.
+enum MaskKind : int { kMaskDynamic = 0, kMaskNoop = 1, kMaskCausalOnly = 2, kMaskSlidingOnly = 3,
+                      kMaskDocCausal = 4 };
+
+__device__ __forceinline__ bool hash_mask_eval(uint64_t seed, int density, int b, int h, int q,
+                                               int kv) {
+  // tests/test_support.hpp:16-29
+  uint64_t x = seed;
+  x ^= 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(b + 1);
+  x ^= 0xc2b2ae3d27d4eb4full * static_cast<uint64_t>(h + 1);
+  x ^= 0x165667b19e3779f9ull * static_cast<uint64_t>(q + 1);
+  x ^= 0x27d4eb2f165667c5ull * static_cast<uint64_t>(kv + 1);
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return static_cast<int>(x & 0xff) < density;
+}
+
+template <int K>
+struct MaskFn {
+  MaskParams p;
+  __device__ __forceinline__ bool operator()(int b, int h, int q, int kv) const {
+    const int qq = q + p.q_offset;  // offset_mask, mask_library.cpp:106-110
+    if constexpr (K == kMaskNoop) {
+      return true;
+    } else if constexpr (K == kMaskCausalOnly) {
+      return qq >= kv;  // causal, mask_library.cpp:13-15
+    } else if constexpr (K == kMaskSlidingOnly) {
+      return qq >= kv && qq - kv <= p.window;  // sliding_window, :17-22
+    } else if constexpr (K == kMaskDocCausal) {
+      // and_mask(document_mask(ids), causal()), :24-34 + :94-98. Index range is
+      // validated on the host before launch (the reference throws IndexOutOfRange).
+      return qq >= kv && __ldg(p.doc_ids + qq) == __ldg(p.doc_ids + kv);
+    } else {
+      const uint32_t t = p.terms;
+      bool ok = true;
+      if (t & kMaskNever) ok = false;
+      if (t & kMaskCausal) ok = ok && (qq >= kv);
+      if (t & kMaskSliding) ok = ok && (qq >= kv && qq - kv <= p.window);
+      if (t & kMaskPrefix) ok = ok && (kv < p.prefix || qq >= kv);  // prefix_lm :36-41
+      if ((t & kMaskDocument) && ok) ok = __ldg(p.doc_ids + qq) == __ldg(p.doc_ids + kv);
+      if ((t & kMaskHash) && ok) ok = hash_mask_eval(p.hash_seed, p.hash_density, b, h, qq, kv);
+      return ok;
+    }
+  }
+};
+
+enum : uint32_t { kScoreAlibi = 1u << 0, kScoreSoftCap = 1u << 1 };
+
+// K is the exact term set: 0 noop, 1 alibi, 2 soft_cap, 3 soft_cap(alibi(s)).
+// Precise selects tanhf (fp32 paths) over the MUFU tanh.approx (bf16 paths).
+template <int K, bool Precise = false>
+struct ScoreFn {
+  ScoreParams p;
+  static constexpr bool kIdentity = (K == 0);
+  __device__ __forceinline__ float apply(float s, int b, int h, int q, int kv) const {
+    (void)b;
+    if constexpr (K & kScoreAlibi) {  // alibi, mask_library.cpp:61-63 (slope of q-head h)
+      s = fmaf(__ldg(p.slopes + h), static_cast<float>(q + p.q_offset - kv), s);
+    }
+    if constexpr (K & kScoreSoftCap) {  // soft_cap, :88
+      s = p.cap * (Precise ? tanhf(s * p.inv_cap) : tanh_fast(s * p.inv_cap));
+    }
+    return s;
+  }
+  __device__ __forceinline__ float grad(float s, int b, int h, int q, int kv) const {
+    (void)b;
+    if constexpr (K & kScoreSoftCap) {  // 1 - tanh^2 (:89-91) through compose (modifiers.hpp:61-65)
+      if constexpr (K & kScoreAlibi) {
+        s = fmaf(__ldg(p.slopes + h), static_cast<float>(q + p.q_offset - kv), s);
+      }
+      const float t = Precise ? tanhf(s * p.inv_cap) : tanh_fast(s * p.inv_cap);
+      return fmaf(-t, t, 1.0f);
+    } else {
+      return 1.0f;
+    }
+  }
+};
+
+}  // namespace fa

@@ -6,8 +6,9 @@
 // pair of 128-row query tiles (block rows 2p, 2p+1) of one (b, h):
 //   warps 0-3  softmax/correction/epilogue for tile 0   (thread = query row)
 //   warps 4-7  the same for tile 1
-//   warp  8    TMA producer: merges both rows' kv lists (partial + full,
-//              ascending = reference visit order) into a union list in smem,
+//   warp  8    TMA producer: merges both rows' kv lists (partial + full) into a
+//              union list in smem (descending block order; any order is exact
+//              math, descending keeps the running max stable),
 //              then streams Q (once) and K_j, V_j (per visited block) with
 //              cp.async.bulk.tensor into a 2-stage (D=128) ring. Empty blocks
 //              are never loaded.
@@ -54,6 +55,7 @@ struct FwdParams {
   const int32_t* full_idx;
   float scale, scale_log2;
   int npairs, num_items;
+  int* work_counter;  // zeroed before launch; dynamic item scheduler
 };
 
 template <int D>
@@ -71,6 +73,7 @@ struct alignas(1024) Smem {
   uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   int32_t ulist[2][kMaxCols];
   int32_t ulen[2];
+  int32_t uitem[2];   // work item of the buffer, -1 = no more work
   uint64_t q_full[2], q_free[2];
   uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages], kv_empty[Cfg<D>::kStages];
   uint64_t s_full[2], p_full[2], o_full[2];
@@ -141,11 +144,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 8 && lane == 0) {
       // ===================== TMA producer =====================
       int kv_it = 0;
-      int n = 0;
-      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
-        const Item it = decode_item(p, item);
+      for (int n = 0;; ++n) {
+        const int item = n == 0 ? static_cast<int>(blockIdx.x)
+                                : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
         const int buf = n & 1;
         mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
+        if (item >= p.num_items) {
+          sm.uitem[buf] = -1;
+          mbar_arrive(&sm.item_full[buf]);
+          break;
+        }
+        const Item it = decode_item(p, item);
+        sm.uitem[buf] = item;
         // ---- union of the two rows' visit lists (ascending merge) ----
         const int mb = p.bm_b == 1 ? 0 : it.b, mh = p.bm_h == 1 ? 0 : it.h;
         const int r0 = 2 * it.pair, r1 = r0 + 1;
@@ -157,19 +167,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t* fi0 = p.full_idx + s0 * p.cols;
         const int32_t* pi1 = pi0 + p.cols;
         const int32_t* fi1 = fi0 + p.cols;
-        int a = 0, bq = 0, c = 0, d = 0, len = 0;
-        int va = a < np0 ? __ldg(pi0 + a) : 0x7fffffff;
-        int vb = bq < nf0 ? __ldg(fi0 + bq) : 0x7fffffff;
-        int vc = c < np1 ? __ldg(pi1 + c) : 0x7fffffff;
-        int vd = d < nf1 ? __ldg(fi1 + d) : 0x7fffffff;
+        // descending merge: blocks nearest the diagonal first, so the running max is
+        // established early and lazy rescaling of O almost never triggers (ALiBi, causal)
+        int a = np0 - 1, bq = nf0 - 1, c = np1 - 1, d = nf1 - 1, len = 0;
+        int va = a >= 0 ? __ldg(pi0 + a) : -1;
+        int vb = bq >= 0 ? __ldg(fi0 + bq) : -1;
+        int vc = c >= 0 ? __ldg(pi1 + c) : -1;
+        int vd = d >= 0 ? __ldg(fi1 + d) : -1;
         while (true) {
-          const int col = min(min(va, vb), min(vc, vd));
-          if (col == 0x7fffffff) break;
+          const int col = max(max(va, vb), max(vc, vd));
+          if (col < 0) break;
           uint32_t e = static_cast<uint32_t>(col);
-          if (va == col) { e |= kIn0; ++a; va = a < np0 ? __ldg(pi0 + a) : 0x7fffffff; }
-          if (vb == col) { e |= kIn0 | kFull0; ++bq; vb = bq < nf0 ? __ldg(fi0 + bq) : 0x7fffffff; }
-          if (vc == col) { e |= kIn1; ++c; vc = c < np1 ? __ldg(pi1 + c) : 0x7fffffff; }
-          if (vd == col) { e |= kIn1 | kFull1; ++d; vd = d < nf1 ? __ldg(fi1 + d) : 0x7fffffff; }
+          if (va == col) { e |= kIn0; --a; va = a >= 0 ? __ldg(pi0 + a) : -1; }
+          if (vb == col) { e |= kIn0 | kFull0; --bq; vb = bq >= 0 ? __ldg(fi0 + bq) : -1; }
+          if (vc == col) { e |= kIn1; --c; vc = c >= 0 ? __ldg(pi1 + c) : -1; }
+          if (vd == col) { e |= kIn1 | kFull1; --d; vd = d >= 0 ? __ldg(fi1 + d) : -1; }
           sm.ulist[buf][len++] = static_cast<int32_t>(e);
         }
         sm.ulen[buf] = len;
@@ -226,22 +238,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                   (acc || kk > 0) ? 1u : 0u);
         }
       };
-      for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
+      for (;; ++n) {
         const int buf = n & 1;
         mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+        if (sm.uitem[buf] < 0) break;
         const int len = sm.ulen[buf];
         const uint32_t* U = reinterpret_cast<const uint32_t*>(sm.ulist[buf]);
         mbar_wait(&sm.q_full[0], n & 1);
         mbar_wait(&sm.q_full[1], n & 1);
         tc_fence_after();
+        // last step that reads Q_t: Q_t's smem is released (q_free) as soon as that QK completes
+        int last_qk[2] = {-1, -1};
+        for (int j = 0; j < len; ++j) {
+          if (U[j] & kIn0) last_qk[0] = j;
+          if (U[j] & kIn1) last_qk[1] = j;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (last_qk[t] < 0) umma_commit(&sm.q_free[t]);
         bool first_pv[2] = {true, true};
         if (len > 0) {
           const int st0 = kv_it % C::kStages;
           mbar_wait(&sm.k_full[st0], (kv_it / C::kStages) & 1);
           tc_fence_after();
           const uint32_t e0 = U[0];
-          if (e0 & kIn0) issue_qk(0, st0);
-          if (e0 & kIn1) issue_qk(1, st0);
+          if (e0 & kIn0) { issue_qk(0, st0); if (last_qk[0] == 0) umma_commit(&sm.q_free[0]); }
+          if (e0 & kIn1) { issue_qk(1, st0); if (last_qk[1] == 0) umma_commit(&sm.q_free[1]); }
         }
         for (int j = 0; j < len; ++j) {
           const int it_j = kv_it + j;
@@ -269,15 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 k1_ready = true;
               }
               issue_qk(t, st1);
+              if (last_qk[t] == j + 1) umma_commit(&sm.q_free[t]);
             }
           }
           umma_commit(&sm.kv_empty[st]);
         }
         kv_it += len;
-        for (int t = 0; t < 2; ++t) {
-          umma_commit(&sm.o_full[t]);
-          umma_commit(&sm.q_free[t]);
-        }
+        for (int t = 0; t < 2; ++t) umma_commit(&sm.o_full[t]);
         mbar_arrive(&sm.item_empty[buf]);
       }
     }
@@ -293,10 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t full_bit = t == 0 ? kFull0 : kFull1;
     uint32_t s_phase = 0;
     int n = 0;
-    for (int item = blockIdx.x; item < p.num_items; item += gridDim.x, ++n) {
-      const Item it = decode_item(p, item);
+    for (;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+      const int item = sm.uitem[buf];
+      if (item < 0) break;
+      const Item it = decode_item(p, item);
       const int len = sm.ulen[buf];
       const int qi = (2 * it.pair + t) * kTile + row;
       float m = -INFINITY, l = 0.f;
@@ -310,41 +332,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.s_full[t], s_phase);
         s_phase ^= 1;
         tc_fence_after();
-        // pass 1: score_mod (+ mask_mod and bounds in partial blocks), row max.
-        // Modified scores are written back to TMEM unless they are a plain scale.
+        // pass 1: score_mod in the log2 domain (+ mask_mod and bounds in partial blocks),
+        // row max. A plain (identity) score keeps raw scores and scales the max once.
         constexpr bool kPlain = ScoreT::kIdentity;
+        const auto rowc = score.row(it.b, it.h, qi, kv0, p.scale);
         float mx = -INFINITY;
 #pragma unroll 1
         for (int cc = 0; cc < 4; ++cc) {
           const int kvc = kv0 + cc * 32;
-          uint32_t bits = 0xffffffffu;
-          if (!full) {
-            bits = 0;
-#pragma unroll 4
-            for (int i = 0; i < 32; ++i) {
-              const int kv = kvc + i;
-              const bool ok = qi < p.Lq && kv < p.Lkv && mask(it.b, it.h, qi, kv);
-              bits |= static_cast<uint32_t>(ok) << i;
-            }
-          }
+          const auto rc = rowc.shifted(cc * 32);
           uint32_t r[32];
           tmem_ld32(s_tm + cc * 32, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float v;
+          if (full) {
+            tmem_wait_ld();
             if constexpr (kPlain) {
-              v = __uint_as_float(r[i]) * p.scale_log2;
+#pragma unroll
+              for (int i = 0; i < 32; i += 2)
+                mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
             } else {
-              v = score.apply(__uint_as_float(r[i]) * p.scale, it.b, it.h, qi, kvc + i) * kLog2e;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float v = rc.log2(__uint_as_float(r[i]), i);
+                r[i] = __float_as_uint(v);
+                mx = fmaxf(mx, v);
+              }
+              tmem_st32(s_tm + cc * 32, r);
             }
-            v = ((bits >> i) & 1u) ? v : -INFINITY;
-            r[i] = __float_as_uint(v);
-            mx = fmaxf(mx, v);
+          } else {
+            const uint32_t bits = qi < p.Lq ? (mask.bits32(it.b, it.h, qi, kvc) &
+                                               range_bits32(kvc, INT_MIN / 2, p.Lkv - 1))
+                                            : 0u;
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float v = kPlain ? __uint_as_float(r[i]) : rc.log2(__uint_as_float(r[i]), i);
+              v = ((bits >> i) & 1u) ? v : -INFINITY;
+              r[i] = __float_as_uint(v);
+              mx = fmaxf(mx, v);
+            }
+            tmem_st32(s_tm + cc * 32, r);
           }
-          if (!kPlain || !full) tmem_st32(s_tm + cc * 32, r);
         }
-        if (!kPlain || !full) tmem_wait_st();
+        if (!(kPlain && full)) tmem_wait_st();
+        if constexpr (kPlain) mx *= rowc.c;  // c > 0: max commutes with the scale
         // lazy rescale (warp-uniform decision; tcgen05.ld/st are warp-collective)
         const float m_new = fmaxf(m, mx);
         const bool need = (m != -INFINITY) && (m_new > m + kRescaleThreshold);
@@ -364,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (need || m == -INFINITY) m = m_new;
         const float msub = (m == -INFINITY) ? 0.f : m;
         // pass 2: P = exp2(x - m) as packed bf16 into S's first 64 columns (64 scores per step)
-        const float xs = (kPlain && full) ? p.scale_log2 : 1.f;
+        const float xs = kPlain ? rowc.c : 1.f;
         float lsum = 0.f;
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
@@ -398,19 +428,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (any_blocks) {
         const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t r[32];
-          tmem_ld32(o_tm + cc * 32, r);
+        for (int cc = 0; cc < D / 64; ++cc) {
+          uint32_t r0[32], r1[32];
+          tmem_ld32(o_tm + cc * 64, r0);
+          tmem_ld32(o_tm + cc * 64 + 32, r1);
           tmem_wait_ld();
           if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 64);
 #pragma unroll
-            for (int v4 = 0; v4 < 4; ++v4) {
+            for (int v4 = 0; v4 < 8; ++v4) {
+              const uint32_t* r = v4 < 4 ? r0 : r1;
+              const int o = (v4 & 3) * 8;
               uint4 w;
-              w.x = pack_bf16(__uint_as_float(r[v4 * 8 + 0]) * inv, __uint_as_float(r[v4 * 8 + 1]) * inv);
-              w.y = pack_bf16(__uint_as_float(r[v4 * 8 + 2]) * inv, __uint_as_float(r[v4 * 8 + 3]) * inv);
-              w.z = pack_bf16(__uint_as_float(r[v4 * 8 + 4]) * inv, __uint_as_float(r[v4 * 8 + 5]) * inv);
-              w.w = pack_bf16(__uint_as_float(r[v4 * 8 + 6]) * inv, __uint_as_float(r[v4 * 8 + 7]) * inv);
+              w.x = pack_bf16(__uint_as_float(r[o + 0]) * inv, __uint_as_float(r[o + 1]) * inv);
+              w.y = pack_bf16(__uint_as_float(r[o + 2]) * inv, __uint_as_float(r[o + 3]) * inv);
+              w.z = pack_bf16(__uint_as_float(r[o + 4]) * inv, __uint_as_float(r[o + 5]) * inv);
+              w.w = pack_bf16(__uint_as_float(r[o + 6]) * inv, __uint_as_float(r[o + 7]) * inv);
               dst[v4] = w;
             }
           }
@@ -472,6 +505,17 @@ fa_status make_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
   return FA_OK;
 }
 
+// One scheduler counter per device, zeroed on the stream before every launch.
+int* work_counter() {
+  static int* counters[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (counters[dev] == nullptr && cudaMalloc(&counters[dev], 256) != cudaSuccess) return nullptr;
+  return counters[dev];
+}
+
 template <int D, class MaskT, class ScoreT>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
               const BmView& bm, MaskT mask, ScoreT score, cudaStream_t st) {
@@ -490,6 +534,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   p.scale_log2 = g.scale * kLog2e;
   p.npairs = (g.rows + 1) / 2;
   p.num_items = g.B * g.Hq * p.npairs;
+  p.work_counter = work_counter();
+  FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "forward: cannot allocate the scheduler counter");
+  FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
   const size_t smem = sizeof(Smem<D>) + 1024;
   auto kern = flex_fwd_sm100_kernel<D, MaskT, ScoreT>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -12,6 +12,7 @@
 // (mask_library.cpp) and are what the C ABI dispatches to.
 #pragma once
 
+#include <limits.h>
 #include <stdint.h>
 
 #include "sm100_ptx.cuh"
@@ -65,9 +66,37 @@ __device__ __forceinline__ bool hash_mask_eval(uint64_t seed, int density, int b
   return static_cast<int>(x & 0xff) < density;
 }
 
+// Bit i of the result = mask(b, h, q, kv0 + i) for i in [0, 32).
+template <class MaskT>
+__device__ __forceinline__ uint32_t mask_bits32_generic(const MaskT& m, int b, int h, int q, int kv0) {
+  uint32_t bits = 0;
+#pragma unroll 4
+  for (int i = 0; i < 32; ++i) bits |= static_cast<uint32_t>(m(b, h, q, kv0 + i)) << i;
+  return bits;
+}
+// Bits set for kv0 + i in [lo, hi] (inclusive), i in [0, 32).
+__device__ __forceinline__ uint32_t range_bits32(int kv0, int lo, int hi) {
+  const int a = max(lo - kv0, 0), e = min(hi - kv0, 31);
+  if (a > e) return 0u;
+  const uint32_t upto = (e >= 31) ? 0xffffffffu : ((2u << e) - 1u);
+  return upto & ~((1u << a) - 1u);
+}
+
 template <int K>
 struct MaskFn {
   MaskParams p;
+  __device__ __forceinline__ uint32_t bits32(int b, int h, int q, int kv0) const {
+    const int qq = q + p.q_offset;
+    if constexpr (K == kMaskNoop) {
+      return 0xffffffffu;
+    } else if constexpr (K == kMaskCausalOnly) {
+      return range_bits32(kv0, INT_MIN / 2, qq);
+    } else if constexpr (K == kMaskSlidingOnly) {
+      return range_bits32(kv0, qq - p.window, qq);
+    } else {
+      return mask_bits32_generic(*this, b, h, q, kv0);
+    }
+  }
   __device__ __forceinline__ bool operator()(int b, int h, int q, int kv) const {
     const int qq = q + p.q_offset;  // offset_mask, mask_library.cpp:106-110
     if constexpr (K == kMaskNoop) {
@@ -111,6 +140,56 @@ struct ScoreFn {
       s = p.cap * (Precise ? tanhf(s * p.inv_cap) : tanh_fast(s * p.inv_cap));
     }
     return s;
+  }
+  // Row context: log2e * apply(s_raw * scale, b, h, q, kv0 + i) for a fixed (b, h, q, kv0),
+  // with every per-row constant hoisted (ALiBi folds into two FFMAs per score).
+  struct Row {
+    float c;      // multiplier of the raw score
+    float base;   // additive term at i = 0 (alibi), pre-scaled
+    float step;   // additive change per kv step (alibi), pre-scaled
+    float outer;  // soft-cap output multiplier (cap * log2e)
+    // the same row context advanced by `off` kv positions (keeps per-score i immediate)
+    __device__ __forceinline__ Row shifted(int off) const {
+      Row r = *this;
+      r.base = fmaf(step, static_cast<float>(off), base);
+      return r;
+    }
+    __device__ __forceinline__ float log2(float s_raw, int i) const {
+      if constexpr (K == 0) {
+        return s_raw * c;
+      } else if constexpr (K == 1) {
+        return fmaf(s_raw, c, fmaf(step, static_cast<float>(i), base));
+      } else if constexpr (K == 2) {
+        return outer * (Precise ? tanhf(s_raw * c) : tanh_fast(s_raw * c));
+      } else {
+        const float t = fmaf(s_raw, c, fmaf(step, static_cast<float>(i), base));
+        return outer * (Precise ? tanhf(t) : tanh_fast(t));
+      }
+    }
+  };
+  __device__ __forceinline__ Row row(int b, int h, int q, int kv0, float scale) const {
+    (void)b;
+    constexpr float kL2e = 1.4426950408889634f;
+    Row r{};
+    float slope = 0.f;
+    if constexpr ((K & kScoreAlibi) != 0) slope = __ldg(p.slopes + h);
+    const float dq = static_cast<float>(q + p.q_offset - kv0);
+    if constexpr (K == 0) {
+      r.c = scale * kL2e;
+    } else if constexpr (K == 1) {
+      r.c = scale * kL2e;
+      r.base = slope * dq * kL2e;
+      r.step = -slope * kL2e;
+    } else if constexpr (K == 2) {
+      r.c = scale * p.inv_cap;
+      r.outer = p.cap * kL2e;
+    } else {
+      r.c = scale * p.inv_cap;
+      r.base = slope * dq * p.inv_cap;
+      r.step = -slope * p.inv_cap;
+      r.outer = p.cap * kL2e;
+    }
+    return r;
   }
   __device__ __forceinline__ float grad(float s, int b, int h, int q, int kv) const {
     (void)b;

@@ -54,19 +54,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
 static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity);
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded wait: try_wait suspends in hardware until the phase flips (or the hint
+// expires); a protocol bug traps after ~20 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t spins = 0;
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1u << 26)) mbar_timeout(bar, parity);
+    if (global_ns() - t0 > 20000000000ull) mbar_timeout(bar, parity);
   }
 }
 static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {

@@ -214,7 +214,8 @@ size_t fa_bwd_workspace_size(int64_t batch, int64_t heads, int64_t q_len, int64_
   // dq accumulator (fp32) + delta (fp32) + log2-domain lse (fp32), 256-byte aligned pieces
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t rows = static_cast<size_t>(batch * heads * q_len);
-  return al(rows * dim * 4) + al(rows * 4) + al(rows * 4);
+  const size_t prow = static_cast<size_t>(batch * heads * ((q_len + 127) / 128 * 128));
+  return al(rows * dim * 4) + al(prow * 4) + al(prow * 4);
 }
 
 fa_status fa_flex_bwd(const fa_bwd_args* a, void* stream) {

@@ -36,6 +36,18 @@
 #include "sm100_ptx.cuh"
 
 namespace fa {
+
+// One scheduler counter per (device, kernel slot), zeroed on the stream before every launch.
+int* scheduler_counter(int slot) {
+  static int* counters[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (counters[dev] == nullptr && cudaMalloc(&counters[dev], 256) != cudaSuccess) return nullptr;
+  return counters[dev] + (slot & 63);
+}
+
 namespace {
 
 constexpr int kThreads = 320;  // 8 softmax warps + producer + MMA; <= 200 regs/thread
@@ -359,9 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_st32(s_tm + cc * 32, r);
             }
           } else {
-            const uint32_t bits = qi < p.Lq ? (mask.bits32(it.b, it.h, qi, kvc) &
-                                               range_bits32(kvc, INT_MIN / 2, p.Lkv - 1))
-                                            : 0u;
+            const uint32_t bits = qi < p.Lq ? mask.bits32(it.b, it.h, qi, kvc, p.Lkv) : 0u;
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -505,17 +515,6 @@ fa_status make_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
   return FA_OK;
 }
 
-// One scheduler counter per device, zeroed on the stream before every launch.
-int* work_counter() {
-  static int* counters[64] = {nullptr};
-  static std::mutex mu;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (counters[dev] == nullptr && cudaMalloc(&counters[dev], 256) != cudaSuccess) return nullptr;
-  return counters[dev];
-}
-
 template <int D, class MaskT, class ScoreT>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
               const BmView& bm, MaskT mask, ScoreT score, cudaStream_t st) {
@@ -534,7 +533,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   p.scale_log2 = g.scale * kLog2e;
   p.npairs = (g.rows + 1) / 2;
   p.num_items = g.B * g.Hq * p.npairs;
-  p.work_counter = work_counter();
+  p.work_counter = scheduler_counter(0);
   FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "forward: cannot allocate the scheduler counter");
   FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
   const size_t smem = sizeof(Smem<D>) + 1024;
@@ -574,6 +573,19 @@ fa_status by_score(const AttnGeom& g, const void* q, const void* k, const void* 
 }
 
 }  // namespace
+
+CUresult encode_tile_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
+  EncodeTiledFn enc = get_encode();
+  if (enc == nullptr) return CUDA_ERROR_NOT_SUPPORTED;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(len),
+                        static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, static_cast<cuuint64_t>(len) * d * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
 
 bool fwd_sm100_supported(const AttnGeom& g) {
   return (g.D == 128 || g.D == 64) && g.bs_q == kTile && g.bs_kv == kTile && g.cols <= kMaxCols;

@@ -66,12 +66,15 @@ __device__ __forceinline__ bool hash_mask_eval(uint64_t seed, int density, int b
   return static_cast<int>(x & 0xff) < density;
 }
 
-// Bit i of the result = mask(b, h, q, kv0 + i) for i in [0, 32).
+// Bit i of the result = mask(b, h, q, kv0 + i) for i in [0, 32); positions kv >= kv_lim are
+// not evaluated (0), so table-backed masks never read past their tables.
 template <class MaskT>
-__device__ __forceinline__ uint32_t mask_bits32_generic(const MaskT& m, int b, int h, int q, int kv0) {
+__device__ __forceinline__ uint32_t mask_bits32_generic(const MaskT& m, int b, int h, int q, int kv0,
+                                                        int kv_lim) {
   uint32_t bits = 0;
 #pragma unroll 4
-  for (int i = 0; i < 32; ++i) bits |= static_cast<uint32_t>(m(b, h, q, kv0 + i)) << i;
+  for (int i = 0; i < 32; ++i)
+    if (kv0 + i < kv_lim) bits |= static_cast<uint32_t>(m(b, h, q, kv0 + i)) << i;
   return bits;
 }
 // Bits set for kv0 + i in [lo, hi] (inclusive), i in [0, 32).
@@ -85,16 +88,36 @@ __device__ __forceinline__ uint32_t range_bits32(int kv0, int lo, int hi) {
 template <int K>
 struct MaskFn {
   MaskParams p;
-  __device__ __forceinline__ uint32_t bits32(int b, int h, int q, int kv0) const {
+  // kv positions >= kv_lim are reported as 0 (bounds of bound_mask, block_mask.cpp:14-19)
+  __device__ __forceinline__ uint32_t bits32(int b, int h, int q, int kv0, int kv_lim) const {
     const int qq = q + p.q_offset;
     if constexpr (K == kMaskNoop) {
-      return 0xffffffffu;
+      return range_bits32(kv0, INT_MIN / 2, kv_lim - 1);
     } else if constexpr (K == kMaskCausalOnly) {
-      return range_bits32(kv0, INT_MIN / 2, qq);
+      return range_bits32(kv0, INT_MIN / 2, min(qq, kv_lim - 1));
     } else if constexpr (K == kMaskSlidingOnly) {
-      return range_bits32(kv0, qq - p.window, qq);
+      return range_bits32(kv0, qq - p.window, min(qq, kv_lim - 1));
     } else {
-      return mask_bits32_generic(*this, b, h, q, kv0);
+      return mask_bits32_generic(*this, b, h, q, kv0, kv_lim);
+    }
+  }
+  // Bit i = mask(b, h, q0 + i, kv) for i in [0, 32): the backward's (kv row, q columns) view.
+  // q positions >= q_lim are reported as 0 and not evaluated.
+  __device__ __forceinline__ uint32_t bits32_q(int b, int h, int q0, int kv, int q_lim) const {
+    const int qq0 = q0 + p.q_offset;
+    const uint32_t in = range_bits32(q0, INT_MIN / 2, q_lim - 1);
+    if constexpr (K == kMaskNoop) {
+      return in;
+    } else if constexpr (K == kMaskCausalOnly) {
+      return in & range_bits32(qq0, kv, INT_MAX / 2);
+    } else if constexpr (K == kMaskSlidingOnly) {
+      return in & range_bits32(qq0, kv, kv + p.window);
+    } else {
+      uint32_t bits = 0;
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i)
+        if (q0 + i < q_lim) bits |= static_cast<uint32_t>((*this)(b, h, q0 + i, kv)) << i;
+      return bits;
     }
   }
   __device__ __forceinline__ bool operator()(int b, int h, int q, int kv) const {
@@ -190,6 +213,19 @@ struct ScoreFn {
       r.outer = p.cap * kL2e;
     }
     return r;
+  }
+  // apply() and its derivative in one evaluation (one tanh for soft_cap).
+  __device__ __forceinline__ float apply_grad(float s, int b, int h, int q, int kv, float& g) const {
+    (void)b;
+    if constexpr (K & kScoreAlibi) s = fmaf(__ldg(p.slopes + h), static_cast<float>(q + p.q_offset - kv), s);
+    if constexpr (K & kScoreSoftCap) {
+      const float t = Precise ? tanhf(s * p.inv_cap) : tanh_fast(s * p.inv_cap);
+      g = fmaf(-t, t, 1.0f);
+      return p.cap * t;
+    } else {
+      g = 1.0f;
+      return s;
+    }
   }
   __device__ __forceinline__ float grad(float s, int b, int h, int q, int kv) const {
     (void)b;

@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native FlexAttention hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+Workload (BASELINE.json configs[1], "C2"): sliding_window(1024) mask_mod + ALiBi score_mod,
+B=4 H=16 S=8192 D=128 bf16, forward + backward. One step = forward + backward over one batch
+with the BlockMask prebuilt (as the reference harness builds it outside the timed region,
+bench.cpp:412-426); the builder is timed separately and reported as `block_mask_us`.
+Metric: effective TFLOPS on unmasked FLOPs (fwd = 4*D*N_live, fwd+bwd = 3.5x fwd), whole job.
+
+Multi-GPU (torchrun, one process per GPU): every rank runs its own C2 batch (weak scaling;
+the path shards by (batch x head) with no collective); time = max over ranks.
+`--impl reference` times the reference CPU implementation (oracle/_ref built from
+/root/reference sources; the C restatement when that is absent) on one (b, h) slice of the
+same workload per step, with all host threads, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ---- workloads (exact unmasked FLOPs measured with the reference builder) ----
+CONFIGS = {
+    "C2": dict(desc="sliding_window(1024)+alibi(alibi_slopes(16)) B4 H16 S8192 D128 bf16 fwd+bwd",
+               B=4, Hq=16, Hkv=16, L=8192, D=128, mask="sliding", score="alibi",
+               fwd_gflop=257.95, live_per_bh=7872000),
+    "C3": dict(desc="and_mask(document_mask(8 docs), causal) B1 H32 S16384 D128 bf16 fwd+bwd",
+               B=1, Hq=32, Hkv=32, L=16384, D=128, mask="doc_causal", score="noop",
+               fwd_gflop=568.85, live_per_bh=34720028),
+    "C4": dict(desc="causal + soft_cap(50) GQA 32/8 B2 S8192 D128 bf16 fwd+bwd",
+               B=2, Hq=32, Hkv=8, L=8192, D=128, mask="causal", score="softcap",
+               fwd_gflop=1099.65, live_per_bh=33558528),
+}
+DOC_LENGTHS = [1004, 350, 639, 2533, 190, 1601, 7058, 3009]
+SEED = 0x5EED0001  # per-config seed S_c (bench.cpp:414); Q/K/V/dO = S_c+1..+4
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic():
+    """dram bytes/launch of the dominant kernel from the committed ncu summary, else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("bwd_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons during the timed region (NVML, else nvidia-smi)."""
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.dev, self.period = device_index, period_s
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    _REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def _sample(self):
+        if self._nvml is not None:
+            p = self._nvml
+            mhz = p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)
+            mask = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.samples.append(mhz)
+            for bit, name in self._REASONS.items():
+                if mask & bit:
+                    self.reasons.add(name)
+            return
+        out = subprocess.run(["nvidia-smi", f"--id={self.dev}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+        f = [x.strip() for x in out.stdout.strip().split(",")]
+        self.samples.append(float(f[0]))
+        self.max_mhz = float(f[1])
+        for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[2:]):
+            if val.lower() == "active":
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- our arm ------------------------------------------------------------------------------
+def build_mods(fa, c, dev):
+    import numpy as np
+    import torch
+    if c["mask"] == "sliding":
+        mask = fa.sliding_window(1024)
+    elif c["mask"] == "causal":
+        mask = fa.causal()
+    else:
+        ids = np.concatenate([np.full(n, i) for i, n in enumerate(DOC_LENGTHS)])
+        mask = fa.and_mask(fa.document_mask(torch.tensor(ids, dtype=torch.int32)), fa.causal())
+    score = {"alibi": fa.alibi(fa.alibi_slopes(c["Hq"])), "softcap": fa.soft_cap(50.0),
+             "noop": fa.noop_score()}[c["score"]]
+    return mask, score
+
+
+def cpu_reference_sample(c, kind_pref="reference"):
+    """Time the reference CPU fwd+bwd on one (b, h) slice of the workload (bounded sample)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    L, D = c["L"], c["D"]
+    q, k, v, do = (O.bf16_round(O.random_f32(SEED + i, (1, 1, L, D))) for i in range(1, 5))
+    if c["mask"] == "sliding":
+        om = O.sliding_window(1024)
+    elif c["mask"] == "causal":
+        om = O.causal()
+    else:
+        ids = np.concatenate([np.full(n, i) for i, n in enumerate(DOC_LENGTHS)])
+        om = O.Mask(terms=O.MASK_DOCUMENT | O.MASK_CAUSAL, doc_ids=ids)
+    if c["score"] == "alibi":
+        os_ = O.Score(terms=O.SCORE_ALIBI, slopes=O.alibi_slopes(c["Hq"])[:1])
+    elif c["score"] == "softcap":
+        os_ = O.Score(terms=O.SCORE_SOFTCAP, cap=50.0)
+    else:
+        os_ = O.Score()
+    cores = os.cpu_count() or 1
+    slice_gflop = 3.5 * c["fwd_gflop"] / (c["B"] * c["Hq"])
+    if O.ref_available() and kind_pref == "reference":
+        fwd_s, bwd_s = O.ref_time_fwd_bwd(q, k, v, do, om, os_, workers=cores)
+        return dict(seconds=fwd_s + bwd_s, fwd_s=fwd_s, bwd_s=bwd_s, cores=cores, kind="reference",
+                    gflop=slice_gflop)
+    # C restatement (single-threaded port) when the reference library is not built
+    bm = O.create_block_mask(om, 1, 1, L, L)
+    t0 = time.perf_counter()
+    o, lse = O.forward(q, k, v, om, os_, bm)
+    t1 = time.perf_counter()
+    O.backward(q, k, v, o, lse, do, om, os_, bm)
+    t2 = time.perf_counter()
+    return dict(seconds=t2 - t0, fwd_s=t1 - t0, bwd_s=t2 - t1, cores=1, kind="port", gflop=slice_gflop)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2412_05496_b200 as fa
+
+    c = CONFIGS[args.config]
+    B, Hq, Hkv, L, D = c["B"], c["Hq"], c["Hkv"], c["L"], c["D"]
+    mask, score = build_mods(fa, c, dev)
+    seed = SEED + 1000003 * rank  # each rank: its own batch of the sharded job
+    q = fa.random_tensor(seed + 1, (B, Hq, L, D), device=dev)
+    k = fa.random_tensor(seed + 2, (B, Hkv, L, D), device=dev)
+    v = fa.random_tensor(seed + 3, (B, Hkv, L, D), device=dev)
+    do = fa.random_tensor(seed + 4, (B, Hq, L, D), device=dev)
+    cfg = fa.AttentionConfig(gqa_group=Hq // Hkv)
+
+    # BlockMask build (timed separately; HBM-tiny, mask-evaluation bound)
+    for _ in range(3):
+        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
+    e1.record()
+    torch.cuda.synchronize()
+    mask_us = e0.elapsed_time(e1) / 10 * 1000.0
+
+    stream = torch.cuda.current_stream()
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    bwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(i=None):
+        if i is not None:
+            fwd_ev[i][0].record(stream)
+        res = fa.forward(q, k, v, score, bm, cfg)
+        if i is not None:
+            fwd_ev[i][1].record(stream)
+            bwd_ev[i][0].record(stream)
+        g = fa.backward(q, k, v, res, do, score, bm, cfg=cfg)
+        if i is not None:
+            bwd_ev[i][1].record(stream)
+        return res, g
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    launches0 = fa.launch_count()
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        torch.cuda.synchronize()
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = fa.launch_count() - launches0
+    ms = t_start.elapsed_time(t_end)
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bwd_ev)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, fwd_ms, bwd_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, fwd_ms, bwd_ms = t.tolist()
+
+    # ---- e2e: same step through the public API with host buffers, H2D + D2H inside ----
+    host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (q, k, v, do)]
+    for h_, d_ in zip(host, (q, k, v, do)):
+        h_.copy_(d_)
+    outs = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (q, q, k, v)]
+    lse_h = torch.empty((B, Hq, L), dtype=torch.float32, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        dq_, dk_, dv_, ddo = (h_.to(dev, non_blocking=True) for h_ in host)
+        res = fa.forward(dq_, dk_, dv_, score, bm, cfg)
+        g = fa.backward(dq_, dk_, dv_, res, ddo, score, bm, cfg=cfg)
+        for o_h, o_d in zip(outs, (res.out, g.dq, g.dk, g.dv)):
+            o_h.copy_(o_d, non_blocking=True)
+        lse_h.copy_(res.lse, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = s0.elapsed_time(s1) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+        barrier()
+    h2d = sum(x.numel() * x.element_size() for x in host)
+    d2h = sum(x.numel() * x.element_size() for x in outs) + lse_h.numel() * 4
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    peak, hbm, peak_kind = peaks()
+    step_gflop = 3.5 * c["fwd_gflop"] * world
+    ms_per_step = ms / args.steps
+    tflops = step_gflop / ms_per_step
+    bwd_gflop = 2.5 * c["fwd_gflop"]
+    achieved = bwd_gflop / bwd_ms  # TFLOP/s of the dominant kernel (backward), per GPU
+    line = {
+        "metric": "effective TFLOPS (unmasked FLOPs) fwd+bwd, C2 sliding_window(1024)+ALiBi",
+        "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: SplitMix64 uniform[-1,1) (random.hpp) generated on device, bf16 RNE",
+        "config": {"workload": f"{args.config}: {c['desc']}", "global_batch": B * world, "seq_len": L,
+                   "heads_q": Hq, "heads_kv": Hkv, "head_dim": D,
+                   "parallelism": f"dp{world}: one (b,h)-shard per GPU, no collective",
+                   "l2": "inputs 4 x 134 MB > 126 MB L2 (no flush needed)",
+                   "block_mask": "built once outside the timed region (builder timed separately)"},
+        "fwd_tflops": round(c["fwd_gflop"] / fwd_ms, 2), "bwd_tflops": round(bwd_gflop / bwd_ms, 2),
+        "fwd_ms": round(fwd_ms, 4), "bwd_ms": round(bwd_ms, 4),
+        "pct_of_peak": round(100.0 * tflops / world / peak, 2), "peak_tflops": peak, "peak_kind": peak_kind,
+        "block_mask_us": round(mask_us, 2),
+        "roofline": {"bound": "tensor", "kernel": "flex_bwd_sm100 (+preprocess/convert)",
+                     "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": profile_traffic(),
+                     "algorithmic_per_launch": f"{bwd_gflop:.2f} GFLOP = 2.5 x 4*D*N_live"},
+        "e2e": {"value": round(step_gflop / e2e_ms, 2), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": int(launches),
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_sample(c)
+            line["cpu_baseline"] = {
+                "value": round(cb["gflop"] / cb["seconds"] / 1000.0, 6), "unit": "TFLOP/s",
+                "cores": cb["cores"], "kind": cb["kind"],
+                "sample": f"one (b,h) slice of {args.config} (1/{B * Hq} of the batch) fwd+bwd, "
+                          f"{cb['seconds']:.2f} s (fwd {cb['fwd_s']:.2f} s, bwd {cb['bwd_s']:.2f} s)"}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "none",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# ---- reference arm ------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    for _ in range(args.warmup):
+        cpu_reference_sample(c)
+    times, cb = [], None
+    for _ in range(args.steps):
+        cb = cpu_reference_sample(c)
+        times.append(cb["seconds"])
+    sec = statistics.median(times)
+    value = cb["gflop"] / sec / 1000.0
+    line = {
+        "impl": "reference",
+        "metric": "effective TFLOPS (unmasked FLOPs) fwd+bwd, C2 sliding_window(1024)+ALiBi",
+        "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1000.0, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: SplitMix64 uniform[-1,1) (random.hpp), bf16-rounded, held as fp32",
+        "config": {"workload": f"{args.config}: {c['desc']}", "sample": "one (b,h) slice per step",
+                   "parallelism": f"BLOCKATTN_WORKERS={cb['cores']} host threads"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cb["cores"], "kind": cb["kind"],
+                         "sample": f"one (b,h) slice of {args.config} (1/{c['B'] * c['Hq']}) fwd+bwd per step"},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -477,3 +477,21 @@ def ref_convert_block_mask(mask: Mask, bd, hd, ql, kl, bs, table: np.ndarray, nu
                                     _p(table, C.c_int32), *[_p(a, C.c_int64) for a in (pn, pi, fn, fi)])
     _check(st, lib)
     return pn, pi, fn, fi
+
+
+def ref_time_fwd_bwd(q, k, v, dout, mask: Mask, score: Score, bs=128, scale=None, gqa=1,
+                     do_bwd=True, workers=None):
+    """Wall time (s) of the reference forward<float> and backward<float> on prebuilt masks."""
+    if workers is not None:
+        os.environ["BLOCKATTN_WORKERS"] = str(int(workers))  # read per call (parallel.cpp:10-15)
+    q, k, v, dout = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v, dout))
+    B, Hq, Hkv, Bkv, Lq, Lkv, D = _dims(q, k, gqa)
+    f, b = C.c_double(0.0), C.c_double(0.0)
+    lib = ref()
+    mc, sc = mask.c(), score.c()
+    ct = C.c_float
+    st = lib.ref_time_fwd_bwd_f32(*[_p(x, ct) for x in (q, k, v, dout)], *_i64(B, Hq, Hkv, Bkv, Lq, Lkv, D),
+                                  C.c_double(scale or 0.0), C.c_int64(gqa), C.byref(sc), C.byref(mc),
+                                  C.c_int64(bs), C.c_int(1 if do_bwd else 0), C.byref(f), C.byref(b))
+    _check(st, lib)
+    return f.value, b.value

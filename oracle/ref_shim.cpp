@@ -342,3 +342,40 @@ int ref_paged_layout(int64_t B, int64_t num_pages, int64_t page_size, uint64_t s
 }
 
 }  // extern "C"
+
+// Timing entry for bench.py's CPU legs: the reference forward and backward on
+// prebuilt masks (create_block_mask/transpose outside the timed region, as
+// bench.cpp:412-426 builds them in build_point), each timed with steady_clock.
+#include <chrono>
+extern "C" int ref_time_fwd_bwd_f32(const float* q, const float* k, const float* v,
+                                    const float* dout, int64_t B, int64_t Hq, int64_t Hkv,
+                                    int64_t Bkv, int64_t Lq, int64_t Lkv, int64_t D, double scale,
+                                    int64_t gqa, const RefScore* s, const RefMask* m, int64_t bs,
+                                    int do_bwd, double* fwd_s, double* bwd_s) {
+  try {
+    AttentionConfig cfg;
+    if (scale > 0) cfg.scale = scale;
+    cfg.gqa_group = gqa;
+    cfg.block_size_q = cfg.block_size_kv = bs;
+    const auto bm = create_block_mask(make_mask(*m), 1, 1, Lq, Lkv, bs, bs);
+    const auto bm_t = transpose(bm);
+    const auto qt = tensor_from(q, B, Hq, Lq, D);
+    const auto kt = tensor_from(k, Bkv, Hkv, Lkv, D);
+    const auto vt = tensor_from(v, Bkv, Hkv, Lkv, D);
+    const auto dot = tensor_from(dout, B, Hq, Lq, D);
+    const auto smod = make_score(*s);
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const auto fwd = forward(qt, kt, vt, smod, bm, cfg);
+    const auto t1 = clk::now();
+    *fwd_s = std::chrono::duration<double>(t1 - t0).count();
+    *bwd_s = 0.0;
+    if (do_bwd) {
+      const auto g = backward(qt, kt, vt, fwd, dot, smod, bm, bm_t, cfg);
+      *bwd_s = std::chrono::duration<double>(clk::now() - t1).count();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}

@@ -567,18 +567,6 @@ def random_tensor(seed: int, shape, dtype=torch.bfloat16, device="cuda", first: 
 
 
 # ---------------------------------------------------------------- paged KV (paged_kv.hpp)
-class _SplitMix64:
-    def __init__(self, seed):
-        self.s = seed & (2**64 - 1)
-
-    def next_u64(self):
-        self.s = (self.s + 0x9E3779B97F4A7C15) & (2**64 - 1)
-        z = self.s
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
-        return z ^ (z >> 31)
-
-
 @dataclass
 class PageTable:
     """PageTable (paged_kv.hpp:18-41), host copy plus device mirrors for the kernels."""
@@ -614,90 +602,63 @@ class PageTable:
 
 
 class PagedKVCache:
-    """PagedKVCache (paged_kv.hpp:50-89): LIFO free list (page 0 first), deterministic shuffle,
-    assign/append/erase with atomic capacity checks. K/V live on the device as
-    (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel."""
-
-    SENTINEL = -1
+    """PagedKVCache (paged_kv.hpp:50-89): host page allocator (paging.PageAllocator: LIFO free
+    list, deterministic shuffle, atomic capacity checks) + device K/V of shape
+    (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel
+    (fa_paged_write, write_tokens paged_kv.cpp:54-70)."""
 
     def __init__(self, batches, num_pages, page_size, kv_heads, dim, dtype=torch.bfloat16,
                  device="cuda"):
-        if batches < 1 or num_pages < 1 or page_size < 1:
-            raise ShapeMismatch("PagedKVCache: batches, num_pages and page_size must be >= 1")
+        from .paging import PageAllocator
+        try:
+            self.alloc = PageAllocator(batches, num_pages, page_size)
+        except ValueError as e:
+            raise ShapeMismatch(str(e)) from None
         self.batches, self.num_pages, self.ps = batches, num_pages, page_size
         self.kv_heads, self.dim = kv_heads, dim
         self.device = torch.device(device)
         self.k = torch.zeros((1, kv_heads, num_pages * page_size, dim), dtype=dtype, device=self.device)
         self.v = torch.zeros_like(self.k)
-        self.table = [self.SENTINEL] * (batches * num_pages)
-        self.p2l = [self.SENTINEL] * num_pages
-        self.owner = [self.SENTINEL] * num_pages
-        self.seq = [0] * batches
-        self.free = [num_pages - 1 - p for p in range(num_pages)]  # LIFO: page 0 popped first
 
     def page_table(self) -> PageTable:
-        return PageTable(self.batches, self.num_pages, self.num_pages, self.ps, list(self.table),
-                         list(self.p2l), list(self.owner), list(self.seq))
+        a = self.alloc
+        return PageTable(self.batches, self.num_pages, self.num_pages, self.ps, list(a.table),
+                         list(a.phys_to_logical), list(a.owner), list(a.seq))
 
     def shuffle_free_pages(self, seed: int):
-        """deterministic_shuffle (random.hpp:49-56)."""
-        rng = _SplitMix64(seed)
-        v = self.free
-        for i in range(len(v), 1, -1):
-            j = rng.next_u64() % i
-            v[i - 1], v[j] = v[j], v[i - 1]
+        self.alloc.shuffle_free_pages(seed)
 
     def _check_batch(self, b):
-        if b < 0 or b >= self.batches:
-            raise IndexOutOfRange(f"PagedKVCache: batch {b} outside [0, {self.batches})")
-
-    def _take(self, b, lp):
-        page = self.free.pop()
-        self.table[b * self.num_pages + lp] = page
-        self.p2l[page] = lp
-        self.owner[page] = b
+        try:
+            self.alloc.check_batch(b)
+        except IndexError as e:
+            raise IndexOutOfRange(str(e)) from None
 
     def erase(self, b):
         self._check_batch(b)
-        owned = -(-self.seq[b] // self.ps)
-        for lp in range(owned):
-            slot = b * self.num_pages + lp
-            page = self.table[slot]
-            self.table[slot] = self.SENTINEL
-            self.p2l[page] = self.SENTINEL
-            self.owner[page] = self.SENTINEL
-            self.free.append(page)
-        self.seq[b] = 0
+        self.alloc.erase(b)
 
     def assign(self, b, k_tokens, v_tokens):
-        """assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim) or (B', ...) slice."""
+        """assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim)."""
+        from .paging import OutOfPagesError
         self._check_batch(b)
         self._check_tokens(k_tokens, v_tokens)
-        n = k_tokens.shape[2]
-        needed = -(-n // self.ps)
-        owned = -(-self.seq[b] // self.ps)
-        if needed > len(self.free) + owned:
-            raise OutOfPages(f"PagedKVCache: assign of {n} tokens needs {needed} pages, only "
-                             f"{len(self.free) + owned} available")
-        self.erase(b)
-        for lp in range(needed):
-            self._take(b, lp)
-        self.seq[b] = n
+        try:
+            self.alloc.assign(b, k_tokens.shape[2])
+        except OutOfPagesError as e:
+            raise OutOfPages(str(e)) from None
         self._write(b, 0, k_tokens, v_tokens)
 
     def append_tokens(self, b, k_new, v_new):
         """append_tokens (paged_kv.cpp:100-126)."""
+        from .paging import OutOfPagesError
         self._check_batch(b)
         self._check_tokens(k_new, v_new)
-        n = k_new.shape[2]
-        old = self.seq[b]
-        owned, total = -(-old // self.ps), -(-(old + n) // self.ps)
-        if total - owned > len(self.free):
-            raise OutOfPages(f"PagedKVCache: append of {n} tokens needs {total - owned} new pages, "
-                             f"only {len(self.free)} free")
-        for lp in range(owned, total):
-            self._take(b, lp)
-        self.seq[b] = old + n
+        old = self.alloc.seq[b]
+        try:
+            self.alloc.append(b, k_new.shape[2])
+        except OutOfPagesError as e:
+            raise OutOfPages(str(e)) from None
         self._write(b, old, k_new, v_new)
 
     def _check_tokens(self, k_t, v_t):
@@ -712,21 +673,17 @@ class PagedKVCache:
         if n == 0:
             return
         if start % self.ps != 0:
-            # unaligned append: shift tokens into a page-aligned staging buffer
+            # unaligned append: stage the partial first page so the scatter is page-aligned
             pad = start % self.ps
-            ks = torch.zeros((1, self.kv_heads, pad + n, self.dim), dtype=self.k.dtype, device=self.device)
-            vs = torch.zeros_like(ks)
-            first_page = self.table[b * self.num_pages + start // self.ps]
-            base = first_page * self.ps
-            ks[:, :, :pad] = self.k[:, :, base:base + pad]
-            vs[:, :, :pad] = self.v[:, :, base:base + pad]
-            ks[:, :, pad:] = k_t
-            vs[:, :, pad:] = v_t
+            base = self.alloc.lookup(b, start // self.ps) * self.ps
+            ks = torch.cat([self.k[:, :, base:base + pad], k_t.to(self.device, self.k.dtype)], dim=2)
+            vs = torch.cat([self.v[:, :, base:base + pad], v_t.to(self.device, self.v.dtype)], dim=2)
             k_t, v_t, start = ks, vs, start - pad
         lp0 = start // self.ps
         npages = -(-k_t.shape[2] // self.ps)
-        row = self.table[b * self.num_pages + lp0: b * self.num_pages + lp0 + npages]
-        pt = PageTable(1, npages, self.num_pages, self.ps, row, self.p2l, self.owner, [k_t.shape[2]])
+        row = self.alloc.table[b * self.num_pages + lp0: b * self.num_pages + lp0 + npages]
+        pt = PageTable(1, npages, self.num_pages, self.ps, row, self.alloc.phys_to_logical,
+                       self.alloc.owner, [k_t.shape[2]])
         cpt = pt.c(self.device)
         lib = _lib.load()
         for src, dst in ((k_t, self.k), (v_t, self.v)):
@@ -743,10 +700,10 @@ class PagedKVCache:
 
     def seq_len(self, b):
         self._check_batch(b)
-        return self.seq[b]
+        return self.alloc.seq[b]
 
     def free_pages(self):
-        return len(self.free)
+        return len(self.alloc.free)
 
     def max_tokens(self):
         return self.num_pages * self.ps

@@ -5,7 +5,7 @@
 //   1. preprocess: Δ_i = Σ_d dO·O (engine.cpp:218-235), lse in log2 units (+inf on
 //      fully masked rows so they contribute exactly nothing, :257-260), padded to
 //      128-row q blocks; dQ accumulator zeroed.
-//   2. main: persistent, warp-specialised CTA (320 threads). A work item is one
+//   2. main: persistent, warp-specialised CTA (512 threads). A work item is one
 //      128-row kv block of one (kv batch, kv head) — the dK/dV pass of the
 //      reference (:307-395): it loops the kv-batch broadcast and the G query
 //      heads of the group and walks the transposed (q-side) lists, so dK and dV
@@ -19,10 +19,13 @@
 //        MMA3 dV += P^T dO            (TS, dO MN-major)
 //        MMA4 dK += dS^T Q            (TS, Q MN-major)
 //        MMA5 dQ_blk = dS K           (SS, both MN-major) into the dP^T columns
-//        compute warps: dQ_blk -> red.global.add.v4.f32 into the fp32 dQ accumulator
+//        reduce warps: dQ_blk -> red.global.add.v4.f32 into the fp32 dQ accumulator
 //      (the fused form of the reference's separate dQ pass, :237-305).
-//      Warp 8 = TMA producer (K/V once per item; Q, dO, lse, Δ per q block,
-//      2-stage ring), warp 9 = MMA issuer.
+//      Warps 0-7 = compute (two warpgroups, 64 q columns each); warps 8-11 = dQ
+//      reduction (pull the dQ tile out of TMEM, release it, red.add while the next
+//      block runs) and the dK/dV epilogue; warp 12 = TMA producer (K/V once per
+//      item; Q, dO, lse, Δ per q block, 2-stage ring); warp 13 = MMA issuer.
+//      Register budgets per warpgroup via setmaxnreg (136 / 152 / 80).
 //      TMEM: S^T [0,128)  dP^T/dQ [128,256)  dV [256,256+D)  dK [256+D,256+2D).
 //   3. convert: dQ fp32 -> bf16.
 #include <cuda.h>
@@ -43,7 +46,7 @@ int* scheduler_counter(int slot);
 
 namespace {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 512;  // 2 compute WGs + dQ/epilogue WG + producer/MMA WG
 constexpr int kTile = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -179,24 +182,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_full[s], 1);
       mbar_init(&sm.q_free[s], 1);
       mbar_init(&sm.item_full[s], 1);
-      mbar_init(&sm.item_empty[s], 1 + 8);
+      mbar_init(&sm.item_empty[s], 1 + 8 + 4);
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.dp_full, 1);
     mbar_init(&sm.ds_full, 256);
     mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_free, 256);
+    mbar_init(&sm.dq_free, 128);
     mbar_init(&sm.dkdv_full, 1);
-    mbar_init(&sm.dkdv_free, 256);
+    mbar_init(&sm.dkdv_free, 128);
     fence_barrier_init();
   }
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
   }
-  if (warp == 9) {
+  if (warp == 13) {
     tmem_alloc(&sm.tmem_base, 512);
     tmem_relinquish();
   }
@@ -206,7 +209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = sm.tmem_base;
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
 
-  if (warp == 8) {
+  // Every role ends in its own copy of the teardown so no code is shared between
+  // warpgroups with different setmaxnreg budgets (ptxas allocates per region).
+#define FA_BWD_TEARDOWN()                     \
+  do {                                        \
+    tc_fence_before();                        \
+    __syncthreads();                          \
+    if (warp == 13) {                         \
+      tc_fence_after();                       \
+      tmem_dealloc(tmem, 512);                \
+    }                                         \
+    return;                                   \
+  } while (0)
+  if (warp >= 12) {
+    reg_dealloc<80>();
+  }
+  if (warp == 12) {
     if (lane == 0) {
       // ===================== TMA producer =====================
       int qs_it = 0;
@@ -248,7 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 9) {
+    FA_BWD_TEARDOWN();
+  } else if (warp == 13) {
     if (lane == 0) {
       // ===================== MMA issuer =====================
       constexpr uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);
@@ -329,15 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&sm.kv_free);
       }
     }
-  } else {
-    // ===================== compute warpgroups =====================
-    const int wg = warp >> 2;          // which 64 q columns (and which half of D for dQ/dK/dV)
+    FA_BWD_TEARDOWN();
+  } else if (warp < 8) {
+    // ===================== compute warpgroups: P^T, dS^T =====================
+    reg_alloc<136>();
+    const int wg = warp >> 2;          // which 64 q columns
     const int wq = warp & 3;           // TMEM lane quarter
-    const int j = wq * 32 + lane;      // kv row within the block (S^T/dP^T/dK/dV lanes)
-    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const uint32_t tm = tmem + lane_base;
-    constexpr int kHalfD = D / 2;
-    uint32_t s_ph = 0, dq_ph = 0;
+    const int j = wq * 32 + lane;      // kv row within the block
+    const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    uint32_t s_ph = 0;
     int qs_it = 0;
     for (int n = 0;; ++n) {
       const int buf = n & 1;
@@ -348,48 +367,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (item < 0) break;
       const KvItem it = decode_kv_item(p, item);
       const int kv = it.c * kTile + j;
+      const bool kv_in = kv < p.Lkv;
       TaskIter ti;
       ti.init(p, it);
-      int T = 0, b, h, r;
+      int b, h, r;
       bool full;
       while (ti.next(b, h, r, full)) {
         const int st = qs_it & 1;
         const int q0 = r * kTile + wg * 64;
+        const auto colc = score.col(b, h, q0, kv, p.scale);
         mbar_wait(&sm.s_full, s_ph);
         mbar_wait(&sm.dp_full, s_ph);
         s_ph ^= 1;
         mbar_wait(&sm.q_full[st], (qs_it >> 1) & 1);  // lse2 / delta of this q block
         tc_fence_after();
-        const bool kv_in = kv < p.Lkv;
         uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
-        // two halves of 32 q columns each keep ~100 registers live
+        // two halves of 32 q columns keep ~100 registers live
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
           const int qc = q0 + hh * 32;
+          const auto cc = colc.shifted(hh * 32);
           uint32_t sr[32], dpr[32];
           tmem_ld32(tm + kS + wg * 64 + hh * 32, sr);
           tmem_ld32(tm + kDP + wg * 64 + hh * 32, dpr);
           // mask bits for this kv row over the 32 q columns (bounds folded in)
           const uint32_t bits = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, qc, kv, p.Lq) : 0u);
-          const float* lse2 = sm.lse2[st] + wg * 64 + hh * 32;
-          const float* dlt = sm.delta[st] + wg * 64 + hh * 32;
+          const float4* lse4 = reinterpret_cast<const float4*>(sm.lse2[st] + wg * 64 + hh * 32);
+          const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[st] + wg * 64 + hh * 32);
           tmem_wait_ld();
           uint32_t pp[16], dsp[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float pv[2], dv2[2];
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 l4 = lse4[i4], d4 = dlt4[i4];
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+            float pv[4], dsv[4];
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int ii = i + e;
-              const float sc = __uint_as_float(sr[ii]) * p.scale;
+            for (int e = 0; e < 4; ++e) {
+              const int ii = i4 * 4 + e;
               float g;
-              const float x = score.apply_grad(sc, b, h, qc + ii, kv, g);
-              const float pr = ((bits >> ii) & 1u) ? ex2(fmaf(x, kLog2e, -lse2[ii])) : 0.f;
+              const float x = cc.log2_grad(__uint_as_float(sr[ii]), ii, g);
+              const float pr = ((bits >> ii) & 1u) ? ex2(x - lv[e]) : 0.f;
               pv[e] = pr;
-              dv2[e] = pr * (__uint_as_float(dpr[ii]) - dlt[ii]) * g * p.scale;
+              dsv[e] = pr * (__uint_as_float(dpr[ii]) - dv4[e]) * (g * p.scale);
             }
-            pp[i >> 1] = pack_bf16(pv[0], pv[1]);
-            dsp[i >> 1] = pack_bf16(dv2[0], dv2[1]);
+            pp[2 * i4] = pack_bf16(pv[0], pv[1]);
+            pp[2 * i4 + 1] = pack_bf16(pv[2], pv[3]);
+            dsp[2 * i4] = pack_bf16(dsv[0], dsv[1]);
+            dsp[2 * i4 + 1] = pack_bf16(dsv[2], dsv[3]);
           }
           tmem_st16(tm + kS + wg * 64 + hh * 16, pp);    // P^T  over S^T columns already read
           tmem_st16(tm + kDP + wg * 64 + hh * 16, dsp);  // dS^T over dP^T columns already read
@@ -405,75 +429,89 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&sm.ds_full);
-        // dQ_blk rows (lanes = q rows of this block) -> fp32 accumulator
+        ++qs_it;
+      }
+    }
+    FA_BWD_TEARDOWN();
+  } else if (warp < 12) {
+    // ===================== dQ reduction + dK/dV epilogue warpgroup =====================
+    reg_alloc<152>();
+    const int wq = warp & 3;
+    const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    uint32_t dq_ph = 0;
+    for (int n = 0;; ++n) {
+      const int buf = n & 1;
+      mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+      const int item = sm.uitem[buf];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
+      if (item < 0) break;
+      const KvItem it = decode_kv_item(p, item);
+      TaskIter ti;
+      ti.init(p, it);
+      int T = 0, b, h, r;
+      bool full;
+      while (ti.next(b, h, r, full)) {
+        // dQ_blk (lanes = q rows): pull all D columns out of TMEM, release it, then reduce
         mbar_wait(&sm.dq_full, dq_ph);
         dq_ph ^= 1;
         tc_fence_after();
-        {
-          const int qrow = r * kTile + wq * 32 + lane;
-          float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D + wg * kHalfD;
+        uint32_t a[D];
 #pragma unroll
-          for (int cc = 0; cc < kHalfD / 32; ++cc) {
-            uint32_t a[32];
-            tmem_ld32(tm + kDP + wg * kHalfD + cc * 32, a);
-            tmem_wait_ld();
-            if (qrow < p.Lq) {
-#pragma unroll
-              for (int v4 = 0; v4 < 8; ++v4)
-                red_add_v4(dst + cc * 32 + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
-                           __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
-            }
-          }
-        }
+        for (int cc = 0; cc < D / 32; ++cc)
+          tmem_ld32(tm + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&a[cc * 32]));
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&sm.dq_free);
-        ++qs_it;
+        const int qrow = r * kTile + wq * 32 + lane;
+        if (qrow < p.Lq) {
+          float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+#pragma unroll
+          for (int v4 = 0; v4 < D / 4; ++v4)
+            red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
+                       __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
+        }
         ++T;
       }
-      // ---- epilogue: dK, dV rows (thread = kv row), this warpgroup's half of D ----
+      // ---- epilogue: dK, dV rows (lanes = kv rows) ----
       mbar_wait(&sm.dkdv_full, n & 1);
       tc_fence_after();
-      {
-        // TMEM loads are warp-collective: every lane loads, only rows < KV_LEN store
-        const bool kv_ok = kv < p.Lkv;
-        const long long orow = (static_cast<long long>(it.kb) * p.Hkv + it.kh) * p.Lkv + kv;
+      const int kv = it.c * kTile + wq * 32 + lane;
+      const bool kv_ok = kv < p.Lkv;
+      const long long orow = (static_cast<long long>(it.kb) * p.Hkv + it.kh) * p.Lkv + kv;
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        __nv_bfloat16* dst = (which == 0 ? p.dk : p.dv) + orow * D;
+        const uint32_t col = which == 0 ? kDK : kDV;
 #pragma unroll
-        for (int which = 0; which < 2; ++which) {
-          __nv_bfloat16* dst = (which == 0 ? p.dk : p.dv) + orow * D + wg * kHalfD;
-          const uint32_t col = (which == 0 ? kDK : kDV) + wg * kHalfD;
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t v[32];
+          if (T > 0) {  // warp-collective loads: every lane loads, rows >= KV_LEN do not store
+            tmem_ld32(tm + col + cc * 32, v);
+            tmem_wait_ld();
+          } else {
 #pragma unroll
-          for (int cc = 0; cc < kHalfD / 32; ++cc) {
-            uint32_t a[32];
-            if (T > 0) {
-              tmem_ld32(tm + col + cc * 32, a);
-              tmem_wait_ld();
-            } else {
+            for (int e = 0; e < 32; ++e) v[e] = 0u;
+          }
+          if (kv_ok) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) a[e] = 0u;
-            }
-            if (kv_ok) {
-              uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
-#pragma unroll
-              for (int v4 = 0; v4 < 4; ++v4)
-                d4[v4] = make_uint4(pack_bf16(__uint_as_float(a[8 * v4]), __uint_as_float(a[8 * v4 + 1])),
-                                    pack_bf16(__uint_as_float(a[8 * v4 + 2]), __uint_as_float(a[8 * v4 + 3])),
-                                    pack_bf16(__uint_as_float(a[8 * v4 + 4]), __uint_as_float(a[8 * v4 + 5])),
-                                    pack_bf16(__uint_as_float(a[8 * v4 + 6]), __uint_as_float(a[8 * v4 + 7])));
-            }
+            for (int q4 = 0; q4 < 4; ++q4)
+              d4[q4] = make_uint4(pack_bf16(__uint_as_float(v[8 * q4]), __uint_as_float(v[8 * q4 + 1])),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 2]), __uint_as_float(v[8 * q4 + 3])),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 4]), __uint_as_float(v[8 * q4 + 5])),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 6]), __uint_as_float(v[8 * q4 + 7])));
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&sm.dkdv_free);
     }
+    FA_BWD_TEARDOWN();
+  } else {
+    FA_BWD_TEARDOWN();  // warps 14-15: idle
   }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
+#undef FA_BWD_TEARDOWN
 }
 
 // Δ and log2-domain lse, padded to whole q blocks (+inf lse / 0 Δ in the padding).

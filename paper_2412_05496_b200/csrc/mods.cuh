@@ -85,6 +85,26 @@ __device__ __forceinline__ uint32_t range_bits32(int kv0, int lo, int hi) {
   return upto & ~((1u << a) - 1u);
 }
 
+// Bit i = (ids[x0 + i] == doc) for i in [0, 32); vectorised 16-byte loads (the ids of a
+// 32-wide chunk are shared by every thread of the warp, so the loads broadcast).
+__device__ __forceinline__ uint32_t doc_match_bits32(const int32_t* ids, int len, int x0, int doc) {
+  uint32_t bits = 0;
+  if (x0 >= 0 && x0 + 32 <= len && (x0 & 3) == 0) {
+    const int4* v = reinterpret_cast<const int4*>(ids + x0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int4 d = __ldg(v + k);
+      bits |= (static_cast<uint32_t>(d.x == doc) | (static_cast<uint32_t>(d.y == doc) << 1) |
+               (static_cast<uint32_t>(d.z == doc) << 2) | (static_cast<uint32_t>(d.w == doc) << 3))
+              << (4 * k);
+    }
+  } else {
+    for (int i = 0; i < 32; ++i)
+      if (x0 + i >= 0 && x0 + i < len) bits |= static_cast<uint32_t>(__ldg(ids + x0 + i) == doc) << i;
+  }
+  return bits;
+}
+
 template <int K>
 struct MaskFn {
   MaskParams p;
@@ -97,6 +117,11 @@ struct MaskFn {
       return range_bits32(kv0, INT_MIN / 2, min(qq, kv_lim - 1));
     } else if constexpr (K == kMaskSlidingOnly) {
       return range_bits32(kv0, qq - p.window, min(qq, kv_lim - 1));
+    } else if constexpr (K == kMaskDocCausal) {
+      uint32_t bits = range_bits32(kv0, INT_MIN / 2, min(qq, kv_lim - 1));
+      if (bits == 0u) return 0u;
+      const int dq = __ldg(p.doc_ids + qq);
+      return bits & doc_match_bits32(p.doc_ids, p.doc_len, kv0, dq);
     } else {
       return mask_bits32_generic(*this, b, h, q, kv0, kv_lim);
     }
@@ -112,6 +137,10 @@ struct MaskFn {
       return in & range_bits32(qq0, kv, INT_MAX / 2);
     } else if constexpr (K == kMaskSlidingOnly) {
       return in & range_bits32(qq0, kv, kv + p.window);
+    } else if constexpr (K == kMaskDocCausal) {
+      const uint32_t bits = in & range_bits32(qq0, kv, INT_MAX / 2);
+      if (bits == 0u) return 0u;
+      return bits & doc_match_bits32(p.doc_ids, p.doc_len, qq0, __ldg(p.doc_ids + kv));
     } else {
       uint32_t bits = 0;
 #pragma unroll 4
@@ -177,6 +206,18 @@ struct ScoreFn {
       r.base = fmaf(step, static_cast<float>(off), base);
       return r;
     }
+    // log2-domain score and d apply / d s (1 unless soft-capped)
+    __device__ __forceinline__ float log2_grad(float s_raw, int i, float& g) const {
+      if constexpr (K == 0 || K == 1) {
+        g = 1.0f;
+        return log2(s_raw, i);
+      } else {
+        const float u = (K == 2) ? s_raw * c : fmaf(s_raw, c, fmaf(step, static_cast<float>(i), base));
+        const float t = Precise ? tanhf(u) : tanh_fast(u);
+        g = fmaf(-t, t, 1.0f);
+        return outer * t;
+      }
+    }
     __device__ __forceinline__ float log2(float s_raw, int i) const {
       if constexpr (K == 0) {
         return s_raw * c;
@@ -190,6 +231,13 @@ struct ScoreFn {
       }
     }
   };
+  // Column context for the backward's (kv row, q columns) view: the same affine form with q
+  // varying (q = q0 + i) at a fixed kv.
+  __device__ __forceinline__ Row col(int b, int h, int q0, int kv, float scale) const {
+    Row r = row(b, h, q0, kv, scale);
+    r.step = -r.step;
+    return r;
+  }
   __device__ __forceinline__ Row row(int b, int h, int q, int kv0, float scale) const {
     (void)b;
     constexpr float kL2e = 1.4426950408889634f;

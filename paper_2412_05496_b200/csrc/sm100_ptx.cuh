@@ -61,24 +61,32 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity);
+static __device__ __forceinline__ void mbar_timeout(uint64_t* bar, uint32_t parity);
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Bounded wait: try_wait suspends in hardware until the phase flips (or the hint
-// expires); a protocol bug traps after ~20 s instead of hanging the GPU.
+// Bounded wait. try_wait suspends the warp in hardware until the phase flips (or the
+// hint expires), so a waiting warp issues almost nothing; the loop body is kept to
+// try_wait + counter so spinning warps do not steal issue slots from working ones.
+// A protocol bug traps (after >= ~20 s) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = global_ns();
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (global_ns() - t0 > 20000000000ull) mbar_timeout(bar, parity);
+    if ((++spins & 0x3FFu) == 0) {
+      const uint64_t t = global_ns();
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) mbar_timeout(bar, parity);
+    }
   }
 }
-static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
-  printf("fa: mbarrier timeout block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar,
-         parity);
+// No printf here: a device call would pin every setmaxnreg region to the ABI register budget.
+static __device__ __forceinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
+  (void)bar;
+  (void)parity;
   __trap();
 }
 

@@ -32,6 +32,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -65,7 +67,20 @@ struct BwdParams {
   float scale;
   int num_items;
   int* work_counter;
+  long long* trace;  // debug only (FA_BWD_TRACE): per-block phase timestamps of CTA 0
+  int exp_flags;     // debug only (FA_BWD_EXP): 1 = skip dQ reductions
 };
+
+// trace slots: [task][event], events: 0 compute-start 1 compute-done 2 mma-ds_full 3 mma5-issued
+// 4 dq_free-wait-done 5 reduce-dq_full 6 reduce-released 7 reduce-red-issued
+constexpr int kTraceTasks = 256, kTraceEv = 12;
+__device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
+  if (p.trace != nullptr && blockIdx.x == 0 && task < kTraceTasks) {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    p.trace[task * kTraceEv + ev] = t;
+  }
+}
 
 template <int D>
 struct BCfg {
@@ -273,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_ts = make_idesc_bf16(128, D, 0, 1);
       constexpr uint32_t idesc_mm = make_idesc_bf16(128, D, 1, 1);
+      constexpr uint32_t idesc_mmT = make_idesc_bf16(D, 128, 1, 1);
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
       int qs_it = 0;
       uint32_t ds_ph = 0, mma2_count = 0;
@@ -311,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&sm.ds_full, ds_ph);
           ds_ph ^= 1;
           tc_fence_after();
+          trace_ev(p, qs_it + t, 2);
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
           for (int kk = 0; kk < kTile / 16; ++kk) {  // MMA3: dV += P^T dO
@@ -325,13 +342,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     idesc_ts, (t > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&sm.q_free[st]);
+          if constexpr (D == 128) {
+            // MMA5: dQ_blk^T = K^T dS^T (M = head dim, N = q) over the dP^T columns, so the
+            // reduction warps own one head-dim index each and write coalesced 128-byte lines
 #pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {  // MMA5: dQ_blk = dS K (over the dP^T columns)
-            umma_ss(tmem + kDP, make_sdesc_sw128(ds_addr + kk * 2048, kTile * 128, 1024),
-                    make_sdesc_sw128(k_addr + kk * 2048, C::kChunkBytes, 1024), idesc_mm,
-                    kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < kTile / 16; ++kk)
+              umma_ss(tmem + kDP, make_sdesc_sw128(k_addr + kk * 2048, C::kChunkBytes, 1024),
+                      make_sdesc_sw128(ds_addr + kk * 2048, kTile * 128, 1024), idesc_mmT,
+                      kk > 0 ? 1u : 0u);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < kTile / 16; ++kk)  // MMA5: dQ_blk = dS K (over the dP^T columns)
+              umma_ss(tmem + kDP, make_sdesc_sw128(ds_addr + kk * 2048, kTile * 128, 1024),
+                      make_sdesc_sw128(k_addr + kk * 2048, C::kChunkBytes, 1024), idesc_mm,
+                      kk > 0 ? 1u : 0u);
           }
           umma_commit(&sm.dq_full);
+          trace_ev(p, qs_it + t, 3);
           if (t + 1 < T) {
             const int st1 = (qs_it + t + 1) & 1;
             mbar_wait(&sm.q_full[st1], ((qs_it + t + 1) >> 1) & 1);
@@ -339,7 +366,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_kmajor(kS, k_addr, smem_u32(sm.q[st1]), &sm.s_full);
             mbar_wait(&sm.dq_free, (mma2_count & 1) ^ 1);
             tc_fence_after();
+            trace_ev(p, qs_it + t, 4);
             mma_kmajor(kDP, v_addr, smem_u32(sm.dO[st1]), &sm.dp_full);
+            trace_ev(p, qs_it + t, 11);
             ++mma2_count;
           }
         }
@@ -376,11 +405,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = qs_it & 1;
         const int q0 = r * kTile + wg * 64;
         const auto colc = score.col(b, h, q0, kv, p.scale);
+        if (threadIdx.x == 0) trace_ev(p, qs_it, 8);
         mbar_wait(&sm.s_full, s_ph);
+        if (threadIdx.x == 0) trace_ev(p, qs_it, 9);
         mbar_wait(&sm.dp_full, s_ph);
         s_ph ^= 1;
+        if (threadIdx.x == 0) trace_ev(p, qs_it, 10);
         mbar_wait(&sm.q_full[st], (qs_it >> 1) & 1);  // lse2 / delta of this q block
         tc_fence_after();
+        if (threadIdx.x == 0) trace_ev(p, qs_it, 0);
         uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
         // two halves of 32 q columns keep ~100 registers live
 #pragma unroll 1
@@ -429,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(&sm.ds_full);
+        if (threadIdx.x == 0) trace_ev(p, qs_it, 1);
         ++qs_it;
       }
     }
@@ -439,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wq = warp & 3;
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     uint32_t dq_ph = 0;
+    int red_it = 0;
     for (int n = 0;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -456,21 +491,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.dq_full, dq_ph);
         dq_ph ^= 1;
         tc_fence_after();
-        uint32_t a[D];
+        if (threadIdx.x == 256) trace_ev(p, red_it, 5);
+        uint32_t a[128];
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc)
+        for (int cc = 0; cc < 4; ++cc)
           tmem_ld32(tm + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&a[cc * 32]));
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&sm.dq_free);
-        const int qrow = r * kTile + wq * 32 + lane;
-        if (qrow < p.Lq) {
-          float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+        if (threadIdx.x == 256) trace_ev(p, red_it, 6);
+        if (!(p.exp_flags & 1)) {
+          if constexpr (D == 128) {
+            // lanes = head-dim index d, columns = q rows of the block: per q row the warp's 32
+            // lanes add 32 consecutive floats (one 128-byte line)
+            const int d = wq * 32 + lane;
+            const int q0r = r * kTile;
+            const int nq = min(kTile, p.Lq - q0r);
+            float* base = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + q0r) * D + d;
+            if (nq == kTile) {
 #pragma unroll
-          for (int v4 = 0; v4 < D / 4; ++v4)
-            red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
-                       __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
+              for (int qq = 0; qq < kTile; ++qq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
+            } else {
+#pragma unroll
+              for (int qq = 0; qq < kTile; ++qq)
+                if (qq < nq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
+            }
+          } else {
+            const int qrow = r * kTile + wq * 32 + lane;
+            if (qrow < p.Lq) {
+              float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+#pragma unroll
+              for (int v4 = 0; v4 < D / 4; ++v4)
+                red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
+                           __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
+            }
+          }
         }
+        if (threadIdx.x == 256) trace_ev(p, red_it, 7);
+        ++red_it;
         ++T;
       }
       // ---- epilogue: dK, dV rows (lanes = kv rows) ----
@@ -595,6 +653,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.work_counter = scheduler_counter(1);
   FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "backward: cannot allocate the scheduler counter");
   FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
+  long long* trace = nullptr;
+  if (getenv("FA_BWD_TRACE") != nullptr) {
+    FA_CHECK_CUDA(cudaMalloc(&trace, sizeof(long long) * kTraceTasks * kTraceEv));
+    FA_CHECK_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * kTraceTasks * kTraceEv, st));
+  }
+  p.trace = trace;
+  p.exp_flags = getenv("FA_BWD_EXP") ? atoi(getenv("FA_BWD_EXP")) : 0;
   const size_t smem = sizeof(BSmem<D>);
   auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -603,6 +668,39 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
     kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, mdo, p, mask, score);
     count_launch();
     FA_CHECK_CUDA(cudaGetLastError());
+  }
+  if (trace != nullptr) {  // debug: per-phase cycle deltas of CTA 0, averaged over its blocks
+    long long h[kTraceTasks * kTraceEv];
+    FA_CHECK_CUDA(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FA_CHECK_CUDA(cudaStreamSynchronize(st));
+    cudaFree(trace);
+    double acc[12] = {0};
+    int cnt = 0;
+    for (int t = 1; t + 1 < kTraceTasks; ++t) {
+      const long long* e = h + t * kTraceEv;
+      const long long* en = h + (t + 1) * kTraceEv;
+      if (e[0] == 0 || en[0] == 0 || e[7] == 0) break;
+      acc[0] += e[1] - e[0];    // compute
+      acc[1] += e[2] - e[1];    // ds_full -> MMA sees it
+      acc[2] += e[5] - e[3];    // MMA5 issue -> dQ ready (MMA3..5 execution)
+      acc[3] += e[6] - e[5];    // dQ TMEM load
+      acc[4] += e[4] - e[6];    // dq_free -> MMA2 issue
+      acc[5] += en[0] - e[4];   // MMA2 issue -> next compute start
+      acc[6] += en[0] - e[0];   // period
+      acc[7] += e[7] - e[6];    // red issue
+      acc[8] += e[3] - e[2];    // MMA3..5 issue duration
+      acc[9] += e[11] - e[4];   // MMA2 issue duration
+      acc[10] += en[9] - e[11]; // MMA2 issued -> next s_full seen
+      acc[11] += en[10] - en[9];// s_full -> dp_full
+      ++cnt;
+    }
+    if (cnt > 0)
+      fprintf(stderr,
+              "[bwd trace] blocks=%d cycles: compute %.0f | ds->mma %.0f | mma3-5 %.0f | dq ld %.0f | "
+              "free->mma2 %.0f | mma2->compute %.0f | period %.0f | red issue %.0f | mma3-5 issue %.0f | "
+              "mma2 issue %.0f | mma2 issued->s_full %.0f | s_full->dp_full %.0f\n",
+              cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
+              acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, acc[9] / cnt, acc[10] / cnt, acc[11] / cnt);
   }
   const long long n4 = rows * D / 4;
   dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148LL * 16), 256, 0, st>>>(

@@ -251,6 +251,10 @@ __device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float
                : "memory");
 }
 
+__device__ __forceinline__ void red_add_f32(float* gaddr, float a) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(gaddr), "f"(a) : "memory");
+}
+
 // ---- register budget per warpgroup -------------------------------------------------
 template <uint32_t N>
 __device__ __forceinline__ void reg_alloc() {

@@ -1,0 +1,360 @@
+// flexattn_b200.hpp — C++ host API mirroring the reference's blockattn API
+// (/root/reference/proj/include/blockattn/*.hpp) over the C ABI in flexattn_b200.h.
+//
+// Header-only. Same names and argument meaning as the reference, so a blockattn user
+// switches by changing the namespace and moving tensors to the device:
+//
+//   blockattn::create_block_mask(mask, b, h, q, kv, bsq, bskv)  block_mask.hpp:109-110
+//   blockattn::transpose(bm)                                   block_mask.hpp:115
+//   blockattn::forward<Real>(q, k, v, smod, bm, cfg)            engine.hpp:68-71
+//   blockattn::backward<Real>(q, k, v, fwd, dout, smod, bm, bm_t, cfg) engine.hpp:78-82
+//   blockattn::decode<Real>(q, k, v, offset, mask, smod, bm, cfg)      engine.hpp:92-96
+//   blockattn::convert_block_mask(bm, page_table)               paged_kv.hpp:101
+//
+// Differences by design: tensors are device buffers (bf16 or fp32); every call is
+// stream-ordered (default stream unless given); errors are the same exception classes
+// (errors.hpp:11-101) raised from the C ABI status codes. No CPU path exists.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "flexattn_b200.h"
+
+namespace flexattn {
+
+using i64 = std::int64_t;
+
+// ---- errors (errors.hpp:11-101) ------------------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+#define FLEXATTN_ERROR(Name) \
+  class Name : public Error { \
+   public:                    \
+    using Error::Error;       \
+  };
+FLEXATTN_ERROR(ShapeMismatch)
+FLEXATTN_ERROR(NonFiniteInput)
+FLEXATTN_ERROR(IndexOutOfRange)
+FLEXATTN_ERROR(NonPositiveCap)
+FLEXATTN_ERROR(GeometryMismatch)
+FLEXATTN_ERROR(BlockMaskMismatch)
+FLEXATTN_ERROR(StaleStatistics)
+FLEXATTN_ERROR(OffsetOutOfRange)
+FLEXATTN_ERROR(OutOfPages)
+FLEXATTN_ERROR(UnmappedBlock)
+FLEXATTN_ERROR(UnmappedPhysicalIndex)
+FLEXATTN_ERROR(CudaError)
+FLEXATTN_ERROR(Unsupported)
+#undef FLEXATTN_ERROR
+
+inline void check(fa_status s) {
+  if (s == FA_OK) return;
+  const std::string m = fa_last_error();
+  switch (s) {
+    case FA_SHAPE_MISMATCH: throw ShapeMismatch(m);
+    case FA_NON_FINITE_INPUT: throw NonFiniteInput(m);
+    case FA_INDEX_OUT_OF_RANGE: throw IndexOutOfRange(m);
+    case FA_NON_POSITIVE_CAP: throw NonPositiveCap(m);
+    case FA_GEOMETRY_MISMATCH: throw GeometryMismatch(m);
+    case FA_BLOCK_MASK_MISMATCH: throw BlockMaskMismatch(m);
+    case FA_STALE_STATISTICS: throw StaleStatistics(m);
+    case FA_OFFSET_OUT_OF_RANGE: throw OffsetOutOfRange(m);
+    case FA_OUT_OF_PAGES: throw OutOfPages(m);
+    case FA_UNMAPPED_BLOCK: throw UnmappedBlock(m);
+    case FA_UNMAPPED_PHYSICAL_INDEX: throw UnmappedPhysicalIndex(m);
+    case FA_UNSUPPORTED: throw Unsupported(m);
+    default: throw CudaError(m);
+  }
+}
+
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- device memory ---------------------------------------------------------------------------
+struct DeviceBuffer {
+  std::shared_ptr<void> p;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t n) : bytes(n) {
+    void* raw = nullptr;
+    if (n) check_cuda(cudaMalloc(&raw, n), "cudaMalloc");
+    p = std::shared_ptr<void>(raw, [](void* x) { if (x) cudaFree(x); });
+  }
+  void* get() const { return p.get(); }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p.get()); }
+};
+
+enum class DType : int32_t { F32 = FA_F32, BF16 = FA_BF16 };
+
+// Dense device (B, H, L, D) tensor, row-major like Tensor4 (tensor.hpp:20-117).
+struct DeviceTensor4 {
+  DeviceBuffer buf;
+  DType dtype = DType::BF16;
+  i64 b = 0, h = 0, l = 0, d = 0;
+  DeviceTensor4() = default;
+  DeviceTensor4(i64 b_, i64 h_, i64 l_, i64 d_, DType t = DType::BF16)
+      : buf(static_cast<size_t>(b_ * h_ * l_ * d_) * (t == DType::F32 ? 4 : 2)), dtype(t), b(b_), h(h_), l(l_), d(d_) {
+    if (b_ <= 0 || h_ <= 0 || l_ <= 0 || d_ <= 0) throw ShapeMismatch("Tensor4: all dims must be positive");
+  }
+  i64 size() const { return b * h * l * d; }
+  fa_tensor c() const {
+    fa_tensor t{};
+    t.data = buf.get();
+    t.dtype = static_cast<int32_t>(dtype);
+    t.b = b; t.h = h; t.l = l; t.d = d;
+    return t;
+  }
+  bool same_shape(const DeviceTensor4& o) const { return b == o.b && h == o.h && l == o.l && d == o.d; }
+};
+
+// random_tensor (random.hpp:41-46), generated on the device.
+inline DeviceTensor4 random_tensor(std::uint64_t seed, i64 b, i64 h, i64 l, i64 d, DType t = DType::BF16,
+                                   cudaStream_t st = nullptr) {
+  DeviceTensor4 x(b, h, l, d, t);
+  check(fa_fill_uniform(x.buf.get(), static_cast<int32_t>(t), seed, 0, x.size(), st));
+  return x;
+}
+
+// ---- modifiers (modifiers.hpp, mask_library.hpp) -------------------------------------------
+struct MaskMod {
+  fa_mask_desc d{};
+  std::shared_ptr<void> keep;  // device doc-id table
+};
+struct ScoreMod {
+  fa_score_desc d{};
+  std::shared_ptr<void> keep;  // device slopes
+  bool identity() const { return d.terms == 0; }
+};
+
+inline MaskMod noop_mask() { return MaskMod{}; }
+inline MaskMod causal() { MaskMod m; m.d.terms = FA_MASK_CAUSAL; return m; }
+inline MaskMod sliding_window(i64 w) {
+  if (w < 0) throw IndexOutOfRange("sliding_window: window must be >= 0, got " + std::to_string(w));
+  MaskMod m; m.d.terms = FA_MASK_SLIDING_WINDOW; m.d.window = w; return m;
+}
+inline MaskMod prefix_lm(i64 p) {
+  if (p < 0) throw IndexOutOfRange("prefix_lm: prefix_len must be >= 0, got " + std::to_string(p));
+  MaskMod m; m.d.terms = FA_MASK_PREFIX_LM; m.d.prefix = p; return m;
+}
+inline MaskMod document_mask(const std::vector<i64>& ids) {
+  std::vector<int32_t> ids32(ids.begin(), ids.end());
+  DeviceBuffer buf(ids32.size() * 4);
+  check_cuda(cudaMemcpy(buf.get(), ids32.data(), ids32.size() * 4, cudaMemcpyHostToDevice), "doc ids");
+  MaskMod m; m.d.terms = FA_MASK_DOCUMENT; m.d.doc_ids = buf.as<int32_t>();
+  m.d.doc_len = static_cast<i64>(ids.size()); m.keep = buf.p; return m;
+}
+inline MaskMod and_mask(const MaskMod& a, const MaskMod& b) {
+  MaskMod m = a;
+  m.d.terms |= b.d.terms;
+  if (b.d.terms & FA_MASK_SLIDING_WINDOW) m.d.window = b.d.window;
+  if (b.d.terms & FA_MASK_PREFIX_LM) m.d.prefix = b.d.prefix;
+  if (b.d.terms & FA_MASK_DOCUMENT) { m.d.doc_ids = b.d.doc_ids; m.d.doc_len = b.d.doc_len; m.keep = b.keep; }
+  if (b.d.terms & FA_MASK_HASH) { m.d.hash_seed = b.d.hash_seed; m.d.hash_density = b.d.hash_density; }
+  return m;
+}
+inline MaskMod offset_mask(MaskMod m, i64 off) { m.d.q_offset += off; return m; }
+
+inline ScoreMod noop_score() { return ScoreMod{}; }
+inline std::vector<double> alibi_slopes(i64 heads) {
+  if (heads < 1) throw IndexOutOfRange("alibi_slopes: heads must be >= 1");
+  std::vector<double> s(static_cast<size_t>(heads));
+  for (i64 h = 0; h < heads; ++h) s[h] = -std::exp2(-8.0 * static_cast<double>(h + 1) / static_cast<double>(heads));
+  return s;
+}
+inline ScoreMod alibi(const std::vector<double>& slopes) {
+  std::vector<float> f(slopes.begin(), slopes.end());
+  DeviceBuffer buf(f.size() * 4);
+  check_cuda(cudaMemcpy(buf.get(), f.data(), f.size() * 4, cudaMemcpyHostToDevice), "slopes");
+  ScoreMod s; s.d.terms = FA_SCORE_ALIBI; s.d.slopes = buf.as<float>();
+  s.d.num_slopes = static_cast<int32_t>(f.size()); s.keep = buf.p; return s;
+}
+inline ScoreMod soft_cap(double cap) {
+  if (!(cap > 0.0) || !std::isfinite(cap)) throw NonPositiveCap("soft_cap: cap must be finite and > 0");
+  ScoreMod s; s.d.terms = FA_SCORE_SOFT_CAP; s.d.cap = cap; return s;
+}
+inline ScoreMod compose(const ScoreMod& outer, const ScoreMod& inner) {
+  if (outer.identity()) return inner;
+  if (inner.identity()) return outer;
+  if (outer.d.terms == FA_SCORE_SOFT_CAP && inner.d.terms == FA_SCORE_ALIBI) {
+    ScoreMod s = inner; s.d.terms |= FA_SCORE_SOFT_CAP; s.d.cap = outer.d.cap; return s;
+  }
+  throw Unsupported("compose: only soft_cap(alibi(s)) is compiled");
+}
+inline ScoreMod offset_score(ScoreMod s, i64 off) { s.d.q_offset += off; return s; }
+
+// ---- config (config.hpp:16-45) ---------------------------------------------------------------
+struct AttentionConfig {
+  std::optional<double> scale;
+  i64 gqa_group = 1;
+  i64 block_size_q = 128;
+  i64 block_size_kv = 128;
+  double scale_or_default() const { return scale.has_value() ? *scale : 0.0; }
+};
+
+// ---- BlockMask (block_mask.hpp:35-79) --------------------------------------------------------
+struct BlockMask {
+  fa_block_mask c{};
+  DeviceBuffer kv_num, kv_idx, full_num, full_idx, q_num, q_idx, fq_num, fq_idx;
+  MaskMod runtime_mask;
+  bool has_runtime_mask = false;
+  i64 rows() const { return c.rows; }
+  i64 cols() const { return c.cols; }
+};
+
+inline BlockMask create_block_mask(const MaskMod& mask, i64 b_dims, i64 h_dims, i64 q_len, i64 kv_len,
+                                   i64 bs_q = 128, i64 bs_kv = 128, cudaStream_t st = nullptr) {
+  i64 rows = 0, cols = 0;
+  size_t ws = 0;
+  check(fa_block_mask_geometry(b_dims, h_dims, q_len, kv_len, bs_q, bs_kv, &rows, &cols, &ws));
+  BlockMask bm;
+  const size_t nr = static_cast<size_t>(b_dims * h_dims * rows), nc = static_cast<size_t>(b_dims * h_dims * cols);
+  const size_t cells = nr * static_cast<size_t>(cols);
+  bm.kv_num = DeviceBuffer(nr * 4); bm.full_num = DeviceBuffer(nr * 4);
+  bm.kv_idx = DeviceBuffer(cells * 4); bm.full_idx = DeviceBuffer(cells * 4);
+  bm.q_num = DeviceBuffer(nc * 4); bm.fq_num = DeviceBuffer(nc * 4);
+  bm.q_idx = DeviceBuffer(cells * 4); bm.fq_idx = DeviceBuffer(cells * 4);
+  bm.c.kv_num_blocks = bm.kv_num.as<int32_t>(); bm.c.kv_indices = bm.kv_idx.as<int32_t>();
+  bm.c.full_kv_num_blocks = bm.full_num.as<int32_t>(); bm.c.full_kv_indices = bm.full_idx.as<int32_t>();
+  bm.c.q_num_blocks = bm.q_num.as<int32_t>(); bm.c.q_indices = bm.q_idx.as<int32_t>();
+  bm.c.full_q_num_blocks = bm.fq_num.as<int32_t>(); bm.c.full_q_indices = bm.fq_idx.as<int32_t>();
+  DeviceBuffer work(ws ? ws : 1);
+  check(fa_create_block_mask(&mask.d, b_dims, h_dims, q_len, kv_len, bs_q, bs_kv, &bm.c, work.get(), ws, st));
+  check_cuda(cudaStreamSynchronize(st), "create_block_mask");  // workspace freed on return
+  bm.runtime_mask = mask;
+  bm.has_runtime_mask = true;
+  return bm;
+}
+
+// transpose (block_mask.cpp:161-178): the q-side arrays of `bm` viewed as a kv-side mask.
+inline BlockMask transpose(const BlockMask& bm) {
+  BlockMask t = bm;
+  t.c.rows = bm.c.cols; t.c.cols = bm.c.rows; t.c.bs_q = bm.c.bs_kv; t.c.bs_kv = bm.c.bs_q;
+  t.c.q_len = bm.c.kv_len; t.c.kv_len = bm.c.q_len;
+  std::swap(t.c.kv_num_blocks, t.c.q_num_blocks); std::swap(t.c.kv_indices, t.c.q_indices);
+  std::swap(t.c.full_kv_num_blocks, t.c.full_q_num_blocks); std::swap(t.c.full_kv_indices, t.c.full_q_indices);
+  t.has_runtime_mask = false;
+  return t;
+}
+
+// Host copies of the kv-side arrays (for inspection / parity), widened to i64 like the reference.
+struct HostBlockMask {
+  std::vector<i64> partial_num, partial_idx, full_num, full_idx;
+};
+inline HostBlockMask to_host(const BlockMask& bm) {
+  auto copy = [](const int32_t* p, size_t n) {
+    std::vector<int32_t> v(n);
+    check_cuda(cudaMemcpy(v.data(), p, n * 4, cudaMemcpyDeviceToHost), "to_host");
+    return std::vector<i64>(v.begin(), v.end());
+  };
+  const size_t nr = static_cast<size_t>(bm.c.b_dims * bm.c.h_dims * bm.c.rows);
+  const size_t cells = nr * static_cast<size_t>(bm.c.cols);
+  return HostBlockMask{copy(bm.c.kv_num_blocks, nr), copy(bm.c.kv_indices, cells),
+                       copy(bm.c.full_kv_num_blocks, nr), copy(bm.c.full_kv_indices, cells)};
+}
+
+// ---- attention (engine.hpp) --------------------------------------------------------------------
+struct AttentionOutput {
+  DeviceTensor4 out;
+  DeviceBuffer lse;  // (B, H, L) fp32, natural log
+};
+struct Gradients {
+  DeviceTensor4 dq, dk, dv;
+};
+
+inline AttentionOutput forward(const DeviceTensor4& q, const DeviceTensor4& k, const DeviceTensor4& v,
+                               const ScoreMod& smod, const BlockMask& bm, const AttentionConfig& cfg = {},
+                               cudaStream_t st = nullptr) {
+  if (!bm.has_runtime_mask) throw BlockMaskMismatch("forward: block mask has no runtime mask attached");
+  if (bm.c.bs_q != cfg.block_size_q || bm.c.bs_kv != cfg.block_size_kv)
+    throw BlockMaskMismatch("block mask block sizes disagree with config");
+  AttentionOutput res{DeviceTensor4(q.b, q.h, q.l, q.d, q.dtype), DeviceBuffer(static_cast<size_t>(q.b * q.h * q.l) * 4)};
+  fa_fwd_args a{};
+  a.q = q.c(); a.k = k.c(); a.v = v.c(); a.out = res.out.c();
+  a.lse = res.lse.as<float>();
+  a.bm = &bm.c;
+  a.mask = bm.runtime_mask.d;
+  a.score = smod.d;
+  a.scale = cfg.scale_or_default();
+  a.gqa_group = cfg.gqa_group;
+  check(fa_flex_fwd(&a, st));
+  return res;
+}
+
+inline Gradients backward(const DeviceTensor4& q, const DeviceTensor4& k, const DeviceTensor4& v,
+                          const AttentionOutput& fwd, const DeviceTensor4& d_out, const ScoreMod& smod,
+                          const BlockMask& bm, const BlockMask& /*bm_t: q side lives in bm*/,
+                          const AttentionConfig& cfg = {}, cudaStream_t st = nullptr) {
+  if (!bm.has_runtime_mask) throw BlockMaskMismatch("backward: block mask has no runtime mask attached");
+  Gradients g{DeviceTensor4(q.b, q.h, q.l, q.d, q.dtype), DeviceTensor4(k.b, k.h, k.l, k.d, k.dtype),
+              DeviceTensor4(v.b, v.h, v.l, v.d, v.dtype)};
+  const size_t ws = fa_bwd_workspace_size(q.b, q.h, q.l, q.d);
+  DeviceBuffer work(ws);
+  fa_bwd_args a{};
+  a.q = q.c(); a.k = k.c(); a.v = v.c(); a.out = fwd.out.c(); a.d_out = d_out.c();
+  a.lse = fwd.lse.as<float>();
+  a.dq = g.dq.c(); a.dk = g.dk.c(); a.dv = g.dv.c();
+  a.bm = &bm.c;
+  a.mask = bm.runtime_mask.d;
+  a.score = smod.d;
+  a.scale = cfg.scale_or_default();
+  a.gqa_group = cfg.gqa_group;
+  a.workspace = work.get();
+  a.workspace_bytes = ws;
+  check(fa_flex_bwd(&a, st));
+  check_cuda(cudaStreamSynchronize(st), "backward");  // workspace freed on return
+  return g;
+}
+
+inline AttentionOutput decode(const DeviceTensor4& q_step, const DeviceTensor4& k_cache,
+                              const DeviceTensor4& v_cache, i64 offset, const MaskMod& mask,
+                              const ScoreMod& smod, const BlockMask& bm, const AttentionConfig& cfg = {},
+                              const fa_page_table* pt = nullptr, cudaStream_t st = nullptr) {
+  AttentionOutput res{DeviceTensor4(q_step.b, q_step.h, q_step.l, q_step.d, q_step.dtype),
+                      DeviceBuffer(static_cast<size_t>(q_step.b * q_step.h * q_step.l) * 4)};
+  const size_t ws = fa_decode_workspace_size(q_step.b, q_step.h, q_step.l, q_step.d, 0);
+  DeviceBuffer work(ws);
+  fa_decode_args a{};
+  a.q = q_step.c(); a.k_cache = k_cache.c(); a.v_cache = v_cache.c(); a.out = res.out.c();
+  a.lse = res.lse.as<float>();
+  a.bm = &bm.c;
+  a.pt = pt;
+  a.offset = offset;
+  a.mask = mask.d;
+  a.score = smod.d;
+  a.scale = cfg.scale_or_default();
+  a.gqa_group = cfg.gqa_group;
+  a.workspace = work.get();
+  a.workspace_bytes = ws;
+  check(fa_flex_decode(&a, st));
+  check_cuda(cudaStreamSynchronize(st), "decode");
+  return res;
+}
+
+// convert_block_mask (paged_kv.cpp:154-228); page-table arrays on the device.
+inline BlockMask convert_block_mask(const BlockMask& bm, const fa_page_table& pt, cudaStream_t st = nullptr) {
+  BlockMask out;
+  const size_t nr = static_cast<size_t>(pt.batches * bm.c.h_dims * bm.c.rows);
+  const size_t cells = nr * static_cast<size_t>(pt.num_physical_pages);
+  out.kv_num = DeviceBuffer(nr * 4); out.full_num = DeviceBuffer(nr * 4);
+  out.kv_idx = DeviceBuffer(cells * 4); out.full_idx = DeviceBuffer(cells * 4);
+  out.c.kv_num_blocks = out.kv_num.as<int32_t>(); out.c.kv_indices = out.kv_idx.as<int32_t>();
+  out.c.full_kv_num_blocks = out.full_num.as<int32_t>(); out.c.full_kv_indices = out.full_idx.as<int32_t>();
+  check(fa_convert_block_mask(&bm.c, &pt, &out.c, st));
+  out.runtime_mask = bm.runtime_mask;
+  out.has_runtime_mask = bm.has_runtime_mask;
+  return out;
+}
+
+}  // namespace flexattn

@@ -1,0 +1,142 @@
+// C++ host API test (include/flexattn_b200.hpp over the C ABI), mirroring the reference's
+// own C++ tests: BlockMask structure (test_block_mask.cpp:40-92) bit-exact vs the oracle port,
+// forward/backward vs the oracle (SURVEY.md §8d tolerances), error taxonomy (errors.hpp).
+// Built by tests/test_cpp_api.py; runs on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "flexattn_b200.hpp"
+#include "flex_oracle.h"
+
+using namespace flexattn;
+
+static int failures = 0;
+#define EXPECT(cond)                                                   \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                      \
+    }                                                                  \
+  } while (0)
+
+static std::vector<float> to_host_f32(const DeviceTensor4& t) {
+  std::vector<float> out(static_cast<size_t>(t.size()));
+  if (t.dtype == DType::F32) {
+    check_cuda(cudaMemcpy(out.data(), t.buf.get(), out.size() * 4, cudaMemcpyDeviceToHost), "d2h");
+  } else {
+    std::vector<uint16_t> raw(out.size());
+    check_cuda(cudaMemcpy(raw.data(), t.buf.get(), raw.size() * 2, cudaMemcpyDeviceToHost), "d2h");
+    for (size_t i = 0; i < raw.size(); ++i) {
+      uint32_t u = static_cast<uint32_t>(raw[i]) << 16;
+      std::memcpy(&out[i], &u, 4);
+    }
+  }
+  return out;
+}
+
+int main() {
+  // ---- BlockMask: causal 256/64 structure and 1024/128 counts -------------------------------
+  {
+    BlockMask bm = create_block_mask(causal(), 1, 1, 256, 256, 64, 64);
+    HostBlockMask h = to_host(bm);
+    for (int r = 0; r < 4; ++r) {
+      EXPECT(h.full_num[r] == r && h.partial_num[r] == 1 && h.partial_idx[r * 4] == r);
+    }
+    BlockMask c = create_block_mask(causal(), 1, 1, 1024, 1024);
+    HostBlockMask hc = to_host(c);
+    long full = 0, part = 0;
+    for (auto x : hc.full_num) full += x;
+    for (auto x : hc.partial_num) part += x;
+    EXPECT(full == 28 && part == 8);
+    // bit-exact vs the oracle port, all four kv-side arrays incl. zero tails
+    fo_mask om{};
+    om.terms = 1;
+    std::vector<int64_t> pn(8), pi(64), fn(8), fi(64);
+    EXPECT(fo_create_block_mask(&om, 1, 1, 1024, 1024, 128, 128, pn.data(), pi.data(), fn.data(), fi.data()) == 0);
+    EXPECT(hc.partial_num == pn && hc.partial_idx == pi && hc.full_num == fn && hc.full_idx == fi);
+    // transpose view: q side of causal 1024 is the mirror (column c visits rows >= c)
+    BlockMask t = transpose(c);
+    HostBlockMask ht = to_host(t);
+    EXPECT(ht.full_num[0] == 7 && ht.partial_num[7] == 1);
+  }
+  // ---- forward + backward vs the oracle, sliding window + ALiBi, bf16 tcgen05 path ----------
+  {
+    const i64 B = 1, H = 2, L = 384, D = 128;
+    DeviceTensor4 q = random_tensor(11, B, H, L, D), k = random_tensor(12, B, H, L, D),
+                  v = random_tensor(13, B, H, L, D), dout = random_tensor(14, B, H, L, D);
+    const auto slopes = alibi_slopes(H);
+    ScoreMod s = alibi(slopes);
+    BlockMask bm = create_block_mask(sliding_window(200), 1, 1, L, L);
+    AttentionOutput fwd = forward(q, k, v, s, bm);
+    Gradients g = backward(q, k, v, fwd, dout, s, bm, transpose(bm));
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    std::vector<float> qf = to_host_f32(q), kf = to_host_f32(k), vf = to_host_f32(v), df = to_host_f32(dout);
+    std::vector<float> of = to_host_f32(fwd.out), lse(static_cast<size_t>(B * H * L));
+    check_cuda(cudaMemcpy(lse.data(), fwd.lse.get(), lse.size() * 4, cudaMemcpyDeviceToHost), "lse");
+    fo_mask om{};
+    om.terms = 2;
+    om.window = 200;
+    om.bound_q = L;
+    om.bound_kv = L;
+    fo_score os{};
+    os.terms = 1;
+    os.slopes = slopes.data();
+    os.num_slopes = static_cast<int32_t>(H);
+    const i64 R = 3;
+    std::vector<int64_t> pn(R), pi(R * R), fn(R), fi(R * R);
+    fo_create_block_mask(&om, 1, 1, L, L, 128, 128, pn.data(), pi.data(), fn.data(), fi.data());
+    fo_bm obm{1, 1, R, R, 128, 128, pn.data(), pi.data(), fn.data(), fi.data()};
+    std::vector<float> ro(of.size()), rl(lse.size());
+    EXPECT(fo_forward_f32(qf.data(), kf.data(), vf.data(), B, H, H, B, L, L, D, 1.0 / std::sqrt(128.0), 1,
+                          &os, &om, &obm, ro.data(), rl.data()) == 0);
+    double eo = 0, el = 0;
+    for (size_t i = 0; i < ro.size(); ++i) eo = std::fmax(eo, std::fabs(ro[i] - of[i]));
+    for (size_t i = 0; i < rl.size(); ++i) el = std::fmax(el, std::fabs(rl[i] - lse[i]));
+    EXPECT(eo <= 2e-2 && el <= 2e-2);
+    std::vector<int64_t> tpn(R), tpi(R * R), tfn(R), tfi(R * R);
+    fo_transpose(1, 1, R, R, pn.data(), pi.data(), fn.data(), fi.data(), tpn.data(), tpi.data(), tfn.data(), tfi.data());
+    fo_bm obt{1, 1, R, R, 128, 128, tpn.data(), tpi.data(), tfn.data(), tfi.data()};
+    std::vector<float> rdq(qf.size()), rdk(kf.size()), rdv(vf.size());
+    EXPECT(fo_backward_f32(qf.data(), kf.data(), vf.data(), of.data(), lse.data(), df.data(), B, H, H, B, L, L, D,
+                           1.0 / std::sqrt(128.0), 1, &os, &om, &obm, &obt, rdq.data(), rdk.data(), rdv.data()) == 0);
+    auto rel = [](const std::vector<float>& got, const std::vector<float>& want) {
+      double m = 0, w = 0;
+      for (size_t i = 0; i < got.size(); ++i) {
+        m = std::fmax(m, std::fabs(got[i] - want[i]));
+        w = std::fmax(w, std::fabs(want[i]));
+      }
+      return m / std::fmax(1.0, w);
+    };
+    EXPECT(rel(to_host_f32(g.dq), rdq) <= 2e-2);
+    EXPECT(rel(to_host_f32(g.dk), rdk) <= 2e-2);
+    EXPECT(rel(to_host_f32(g.dv), rdv) <= 2e-2);
+    std::printf("forward max|dO| %.3g lse %.3g\n", eo, el);
+  }
+  // ---- error taxonomy ---------------------------------------------------------------------------
+  {
+    bool thrown = false;
+    try { sliding_window(-1); } catch (const IndexOutOfRange&) { thrown = true; }
+    EXPECT(thrown);
+    thrown = false;
+    try { soft_cap(0.0); } catch (const NonPositiveCap&) { thrown = true; }
+    EXPECT(thrown);
+    thrown = false;
+    try {
+      DeviceTensor4 q = random_tensor(1, 1, 2, 256, 128), k = random_tensor(2, 1, 2, 256, 64);
+      BlockMask bm = create_block_mask(causal(), 1, 1, 256, 256);
+      forward(q, k, k, noop_score(), bm);
+    } catch (const ShapeMismatch&) { thrown = true; }
+    EXPECT(thrown);
+    thrown = false;
+    try {
+      DeviceTensor4 q = random_tensor(1, 1, 2, 256, 128);
+      BlockMask bm = create_block_mask(causal(), 1, 1, 512, 256);
+      forward(q, q, q, noop_score(), bm);
+    } catch (const BlockMaskMismatch&) { thrown = true; }
+    EXPECT(thrown);
+  }
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}

@@ -9,8 +9,10 @@
 // the K/V tiles; a single thread streams each (K, V) tile pair into a 3-stage
 // shared-memory ring with 1-D cp.async.bulk (a page is contiguous: bs_kv rows
 // of D bf16 per head), completion tracked by mbarrier transaction counts.
-// Warps split the tile's rows; lanes split D (conflict-free 8-byte smem reads);
-// each warp keeps its own online-softmax state; states are merged in smem and,
+// Warps split the tile's rows in 32-key chunks; lanes split D (conflict-free 8-byte smem
+// reads); per chunk a 31-shuffle transposed butterfly turns 32 partial dots into one score
+// per lane, one online-softmax update, then P V with broadcast weights; each warp keeps its
+// own online-softmax state; states are merged in smem and,
 // with more than one split, across splits by a combine kernel.
 //
 // Paged mode: physical page c -> logical page phys_to_logical[c] of owner[c];
@@ -131,54 +133,77 @@ __global__ void __launch_bounds__(128, 1) decode_kernel(DecParams p, MaskT mask,
     const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(sm.kv[s][0]);
     const __nv_bfloat16* vs = reinterpret_cast<const __nv_bfloat16*>(sm.kv[s][1]);
     for (int jb = warp * 32; jb < valid_rows; jb += 128) {
-      const int nj = min(32, valid_rows - jb);
-      for (int jj = 0; jj < nj; ++jj) {
-        const int j = jb + jj;
-        // q . k_j : lanes split D, butterfly reduction leaves the sum in every lane
-        float part = 0.f;
+      // 1) partial dots of this lane's D-slice against the chunk's 32 keys
+      float v[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int j = min(jb + t, valid_rows - 1);  // rows past the page end are masked below
         if constexpr (kPer == 4) {
           const uint2 kw = *reinterpret_cast<const uint2*>(ks + j * D + lane * 4);
           const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(&kw.x);
           const __nv_bfloat162 k23 = *reinterpret_cast<const __nv_bfloat162*>(&kw.y);
-          part = qv[0] * __low2float(k01) + qv[1] * __high2float(k01) +
-                 qv[2] * __low2float(k23) + qv[3] * __high2float(k23);
+          v[t] = qv[0] * __low2float(k01) + qv[1] * __high2float(k01) + qv[2] * __low2float(k23) +
+                 qv[3] * __high2float(k23);
         } else {
           const __nv_bfloat162 k01 = *reinterpret_cast<const __nv_bfloat162*>(ks + j * D + lane * 2);
-          part = qv[0] * __low2float(k01) + qv[1] * __high2float(k01);
+          v[t] = qv[0] * __low2float(k01) + qv[1] * __high2float(k01);
         }
+      }
+      // 2) transposed butterfly: 31 shuffles leave lane l with the full dot of key jb + l
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        const int phys = c * tile_rows + j;
-        int logical = phys;
-        bool live = true;
-        if (p.paged) {
-          logical = lpage * tile_rows + j;
-          live = own == b && lpage >= 0 && logical < seq;
-        }
-        float x = score.apply(part * p.scale, b, h, qrow, logical) * kLog2eD;
-        if (!full_blk) live = live && qrow < p.n_new && logical < p.logical_kv && mask(b, h, qrow, logical);
-        if (!live) continue;  // exact zero weight (warp-uniform)
-        if (x > m) {
-          const float alpha = ex2(m - x);  // m = -inf -> 0
-          l *= alpha;
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
 #pragma unroll
-          for (int e = 0; e < kPer; ++e) acc[e] *= alpha;
-          m = x;
+        for (int i = 0; i < off; ++i) {
+          const float send = upper ? v[i] : v[i + off];
+          const float keep = upper ? v[i + off] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
         }
-        const float pw = ex2(x - m);
-        l += pw;
+      }
+      // 3) score_mod / mask_mod for this lane's key, one online-softmax update per chunk
+      const int j = jb + lane;
+      const int phys = c * tile_rows + j;
+      int logical = phys;
+      bool live = j < valid_rows;
+      if (p.paged) {
+        logical = lpage * tile_rows + j;
+        live = live && own == b && lpage >= 0 && logical < seq;
+      }
+      float x = -INFINITY;
+      if (live && (full_blk || (qrow < p.n_new && logical < p.logical_kv && mask(b, h, qrow, logical))))
+        x = score.apply(v[0] * p.scale, b, h, qrow, logical) * kLog2eD;
+      float mx = x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (mx == -INFINITY) continue;  // the whole chunk is masked: exact no-op (warp-uniform)
+      const float m_new = fmaxf(m, mx);
+      const float alpha = ex2(m - m_new);  // m == -inf -> 0
+      const float pw = ex2(x - m_new);     // masked -> 0
+      float ps = pw;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      l = l * alpha + ps;
+      m = m_new;
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) acc[e] *= alpha;
+      // 4) P V: broadcast each key's weight, lanes accumulate their D-slice
+      const int nj = min(32, valid_rows - jb);
+#pragma unroll 8
+      for (int t = 0; t < nj; ++t) {
+        const float pj = __shfl_sync(0xffffffffu, pw, t);
+        const int jj = jb + t;
         if constexpr (kPer == 4) {
-          const uint2 vw = *reinterpret_cast<const uint2*>(vs + j * D + lane * 4);
+          const uint2 vw = *reinterpret_cast<const uint2*>(vs + jj * D + lane * 4);
           const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(&vw.x);
           const __nv_bfloat162 v23 = *reinterpret_cast<const __nv_bfloat162*>(&vw.y);
-          acc[0] = fmaf(pw, __low2float(v01), acc[0]);
-          acc[1] = fmaf(pw, __high2float(v01), acc[1]);
-          acc[2] = fmaf(pw, __low2float(v23), acc[2]);
-          acc[3] = fmaf(pw, __high2float(v23), acc[3]);
+          acc[0] = fmaf(pj, __low2float(v01), acc[0]);
+          acc[1] = fmaf(pj, __high2float(v01), acc[1]);
+          acc[2] = fmaf(pj, __low2float(v23), acc[2]);
+          acc[3] = fmaf(pj, __high2float(v23), acc[3]);
         } else {
-          const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(vs + j * D + lane * 2);
-          acc[0] = fmaf(pw, __low2float(v01), acc[0]);
-          acc[1] = fmaf(pw, __high2float(v01), acc[1]);
+          const __nv_bfloat162 v01 = *reinterpret_cast<const __nv_bfloat162*>(vs + jj * D + lane * 2);
+          acc[0] = fmaf(pj, __low2float(v01), acc[0]);
+          acc[1] = fmaf(pj, __high2float(v01), acc[1]);
         }
       }
     }

@@ -79,7 +79,7 @@ def main(which):
             t = timeit(lambda: fa.decode(q, cache.k_phys(), cache.v_phys(), L - 1, fa.causal(), fa.noop_score(),
                                          pbm, page_table=pt, num_splits=splits))
             gb = 2 * B * H * L * D * 2 / 1e9
-            print(f"C5 decode splits={splits} {t:.3f} ms  {gb / t:.1f} GB/s", flush=True)
+            print(f"C5 decode splits={splits} {t:.3f} ms  {gb / t:.3f} TB/s ({gb / t / 6.5418 * 100:.1f}% of 6541.8 GB/s)", flush=True)
 
 
 if __name__ == "__main__":

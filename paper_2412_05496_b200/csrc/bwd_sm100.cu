@@ -2,31 +2,35 @@
 // accumulate), the tensor-core replacement of backward (engine.cpp:174-401).
 //
 // Kernels (one stream, in order):
-//   1. preprocess: Δ_i = Σ_d dO·O (engine.cpp:218-235), lse in log2 units (+inf on
-//      fully masked rows so they contribute exactly nothing, :257-260), padded to
-//      128-row q blocks; dQ accumulator zeroed.
+//   1. preprocess: Δ_i = Σ_d dO·O (engine.cpp:218-235), stored pre-multiplied by the
+//      softmax scale; lse in log2 units (+inf on fully masked rows so they contribute
+//      exactly nothing, :257-260); both padded to 128-row q blocks.
 //   2. main: persistent, warp-specialised CTA (512 threads). A work item is one
 //      128-row kv block of one (kv batch, kv head) — the dK/dV pass of the
-//      reference (:307-395): it loops the kv-batch broadcast and the G query
-//      heads of the group and walks the transposed (q-side) lists, so dK and dV
-//      accumulate in TMEM for the whole item. Per visited q block:
-//        MMA1 S^T  = K Q^T            (SS, TMEM fp32, 128 x 128)
-//        MMA2 dP^T = V dO^T           (SS)
-//        compute warps (thread = kv row, two warpgroups split the 128 q columns):
-//           P^T  = exp2(score_mod(S^T) - lse)      mask_mod only in partial blocks
-//           dS^T = P^T (dP^T - Δ) score_mod'(s) scale
-//           -> P^T, dS^T as bf16 into TMEM (aliasing S^T / dP^T) and dS^T into smem
-//        MMA3 dV += P^T dO            (TS, dO MN-major)
-//        MMA4 dK += dS^T Q            (TS, Q MN-major)
-//        MMA5 dQ_blk = dS K           (SS, both MN-major) into the dP^T columns
-//        reduce warps: dQ_blk -> red.global.add.v4.f32 into the fp32 dQ accumulator
-//      (the fused form of the reference's separate dQ pass, :237-305).
-//      Warps 0-7 = compute (two warpgroups, 64 q columns each); warps 8-11 = dQ
-//      reduction (pull the dQ tile out of TMEM, release it, red.add while the next
-//      block runs) and the dK/dV epilogue; warp 12 = TMA producer (K/V once per
-//      item; Q, dO, lse, Δ per q block, 2-stage ring); warp 13 = MMA issuer.
-//      Register budgets per warpgroup via setmaxnreg (136 / 152 / 80).
-//      TMEM: S^T [0,128)  dP^T/dQ [128,256)  dV [256,256+D)  dK [256+D,256+2D).
+//      reference (:307-395): it loops the kv-batch broadcast and the G query heads
+//      of the group and walks the transposed (q-side) lists, so dK and dV
+//      accumulate in TMEM for the whole item. Per visited q block t:
+//        S^T  = K Q^T          (SS)             -> TMEM S    [0,128)
+//        dP^T = V dO^T         (SS)             -> TMEM dP   [128,256)
+//        compute warps, phase A (after S^T):  (P·scale)^T = exp2(score_mod(S^T) - lse + log2
+//           scale), mask_mod only in partial blocks, as bf16 into TMEM over S^T (dV is rescaled
+//           by 1/scale in the epilogue); P·scale·mod' kept in registers as packed bf16
+//        compute warps, phase B (after dP^T): dS^T = P (dP^T - Δ) mod' scale (bf16) into
+//           TMEM over dP^T and into smem
+//        dV  += P^T dO          (TS: P^T from TMEM)
+//        dK  += dS^T Q          (TS: dS^T from TMEM)
+//        dQ^T = K^T dS^T        (SS, both MN-major) -> TMEM over the dP columns
+//      The MMA warp software-pipelines consecutive blocks so the tensor core runs the
+//      GEMMs of one block while the compute warps work on the next:
+//          S(t+1) | dK(t) | dQ(t) | dP(t+1) | dV(t+1) | S(t+2) | ...
+//      Shared memory bandwidth (128 B/clk/SM) is the scarce resource: an SS 128x128x16
+//      MMA alone reads 128 B/clk, so the two GEMMs with an operand already in TMEM (dV,
+//      dK) use TS, and dQ (the fused form of the reference's separate dQ pass,
+//      :237-305) goes from TMEM through registers to L2 with red.global.add (lanes = the
+//      head-dim index, so each instruction adds one whole 128-byte line) instead of
+//      being staged through shared memory.
+//      Warps 0-7 compute (two warpgroups, 64 q columns each; thread = kv row),
+//      warps 8-11 dQ reduction + dK/dV epilogue, warp 12 TMA producer, warp 13 MMA.
 //   3. convert: dQ fp32 -> bf16.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -59,7 +63,7 @@ struct BwdParams {
   const int32_t* q_idx;
   const int32_t* fq_num;
   const int32_t* fq_idx;
-  const float* lse2;   // (B*Hq, Lq_pad)
+  const float* lse2;   // (B*Hq, Lq_pad): cterm, see bwd_preprocess_kernel
   const float* delta;  // (B*Hq, Lq_pad)
   float* dq_acc;       // (B*Hq, Lq, D) fp32
   __nv_bfloat16* dk;
@@ -68,17 +72,22 @@ struct BwdParams {
   int num_items;
   int* work_counter;
   long long* trace;  // debug only (FA_BWD_TRACE): per-block phase timestamps of CTA 0
-  int exp_flags;     // debug only (FA_BWD_EXP): 1 = skip dQ reductions
+  int exp_flags;     // debug only (FA_BWD_EXP, wrong results): 1 skip dQ reds
 };
 
-// trace slots: [task][event], events: 0 compute-start 1 compute-done 2 mma-ds_full 3 mma5-issued
-// 4 dq_free-wait-done 5 reduce-dq_full 6 reduce-released 7 reduce-red-issued
-constexpr int kTraceTasks = 256, kTraceEv = 12;
+// trace slots [block][event] of CTA 0 (FA_BWD_TRACE); see the host-side summary in run().
+// Compiled in only with -DFA_BWD_TRACE_BUILD=1 (make EXTRA=-DFA_BWD_TRACE_BUILD=1).
+#ifndef FA_BWD_TRACE_BUILD
+#define FA_BWD_TRACE_BUILD 0
+#endif
+constexpr int kTraceTasks = 256, kTraceEv = 24;
 __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
-  if (p.trace != nullptr && blockIdx.x == 0 && task < kTraceTasks) {
-    long long t;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-    p.trace[task * kTraceEv + ev] = t;
+  if constexpr (FA_BWD_TRACE_BUILD != 0) {
+    if (p.trace != nullptr && blockIdx.x == 0 && task < kTraceTasks) {
+      long long t;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+      p.trace[task * kTraceEv + ev] = t;
+    }
   }
 }
 
@@ -87,6 +96,7 @@ struct BCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kTileBytes = kTile * D * 2;
   static constexpr int kChunkBytes = kTile * 128;
+  static constexpr int kDoStages = 2;
 };
 
 template <int D>
@@ -94,13 +104,14 @@ struct alignas(1024) BSmem {
   uint8_t k[BCfg<D>::kTileBytes];
   uint8_t v[BCfg<D>::kTileBytes];
   uint8_t q[2][BCfg<D>::kTileBytes];
-  uint8_t dO[2][BCfg<D>::kTileBytes];
-  uint8_t ds[kTile * kTile * 2];  // dS^T as the MN-major A operand of MMA5
+  uint8_t dO[BCfg<D>::kDoStages][BCfg<D>::kTileBytes];
+  uint8_t ds[kTile * kTile * 2];  // dS^T [kv][q], SW128, two 64-wide q chunks
   float lse2[2][kTile];
-  float delta[2][kTile];
-  uint64_t kv_full, kv_free;
+  float delta[BCfg<D>::kDoStages][kTile];
+  uint64_t k_full, v_full, k_free, v_free;
   uint64_t q_full[2], q_free[2];
-  uint64_t s_full, dp_full, ds_full, dq_full, dq_free, dkdv_full, dkdv_free;
+  uint64_t do_full[BCfg<D>::kDoStages], do_free[BCfg<D>::kDoStages];
+  uint64_t s_full, p_full, dp_full, ds_full, ds_free, dq_full, dq_empty, dkdv_full, dkdv_free;
   uint64_t item_full[2], item_empty[2];
   int32_t uitem[2];
   uint32_t tmem_base;
@@ -110,8 +121,9 @@ struct KvItem {
   int kb, kh, c;
 };
 __device__ __forceinline__ KvItem decode_kv_item(const BwdParams& p, int item) {
-  const int per = p.Bkv * p.Hkv;
-  const int c = item / per, rem = item % per;  // low kv blocks first: the heaviest for causal masks
+  // kv blocks of one (kv batch, kv head) are consecutive items: the CTAs working at the same
+  // time share their q-side Q/dO tiles through L2 instead of each missing to HBM
+  const int c = item % p.cols, rem = item / p.cols;
   return KvItem{rem / p.Hkv, rem % p.Hkv, c};
 }
 
@@ -181,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     flex_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV,
-                          const __grid_constant__ CUtensorMap tmDO, const BwdParams p, MaskT mask,
+                          const __grid_constant__ CUtensorMap tmDO,
+                          const BwdParams p, MaskT mask,
                           ScoreT score) {
   using C = BCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -191,21 +204,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();  // SWIZZLE_128B operands need 1 KiB alignment
 
   if (threadIdx.x == 0) {
-    mbar_init(&sm.kv_full, 1);
-    mbar_init(&sm.kv_free, 1);
+    mbar_init(&sm.k_full, 1);
+    mbar_init(&sm.v_full, 1);
+    mbar_init(&sm.k_free, 1);
+    mbar_init(&sm.v_free, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.q_full[s], 1);
       mbar_init(&sm.q_free[s], 1);
       mbar_init(&sm.item_full[s], 1);
       mbar_init(&sm.item_empty[s], 1 + 8 + 4);
     }
+    for (int s = 0; s < C::kDoStages; ++s) {
+      mbar_init(&sm.do_full[s], 1);
+      mbar_init(&sm.do_free[s], 1 + 8);  // dV MMA commit + the 8 compute warps (Δ read)
+    }
     mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.p_full, 8);
     mbar_init(&sm.dp_full, 1);
-    mbar_init(&sm.ds_full, 256);
+    mbar_init(&sm.ds_full, 8);
+    mbar_init(&sm.ds_free, 1);
     mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_free, 128);
+    mbar_init(&sm.dq_empty, 4);
     mbar_init(&sm.dkdv_full, 1);
-    mbar_init(&sm.dkdv_free, 128);
+    mbar_init(&sm.dkdv_free, 4);
     fence_barrier_init();
   }
   if (warp == 12 && lane == 0) {
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 12) {
     if (lane == 0) {
       // ===================== TMA producer =====================
-      int qs_it = 0;
+      int blk = 0;
       for (int n = 0;; ++n) {
         const int item = n == 0 ? static_cast<int>(blockIdx.x)
                                 : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
@@ -252,32 +273,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sm.item_full[buf]);
         if (item >= p.num_items) break;
         const KvItem it = decode_kv_item(p, item);
-        mbar_wait(&sm.kv_free, (n & 1) ^ 1);
-        mbar_expect_tx(&sm.kv_full, 2 * C::kTileBytes);
-        for (int ch = 0; ch < C::kChunks; ++ch) {
-          tma_load_3d(sm.k + ch * C::kChunkBytes, &tmK, &sm.kv_full, ch * 64, it.c * kTile,
+        // K first (the item's first GEMM needs it), then V
+        mbar_wait(&sm.k_free, (n & 1) ^ 1);
+        mbar_expect_tx(&sm.k_full, C::kTileBytes);
+        for (int ch = 0; ch < C::kChunks; ++ch)
+          tma_load_3d(sm.k + ch * C::kChunkBytes, &tmK, &sm.k_full, ch * 64, it.c * kTile,
                       it.kb * p.Hkv + it.kh);
-          tma_load_3d(sm.v + ch * C::kChunkBytes, &tmV, &sm.kv_full, ch * 64, it.c * kTile,
-                      it.kb * p.Hkv + it.kh);
-        }
         TaskIter ti;
         ti.init(p, it);
         int b, h, r;
         bool full;
+        bool v_loaded = false;
         while (ti.next(b, h, r, full)) {
-          const int st = qs_it & 1;
-          mbar_wait(&sm.q_free[st], ((qs_it >> 1) & 1) ^ 1);
-          mbar_expect_tx(&sm.q_full[st], 2 * C::kTileBytes + 2 * kTile * 4);
-          for (int ch = 0; ch < C::kChunks; ++ch) {
+          const int st = blk & 1;
+          const long long row0 = static_cast<long long>(b * p.Hq + h) * p.Lq_pad + r * kTile;
+          mbar_wait(&sm.q_free[st], ((blk >> 1) & 1) ^ 1);
+          trace_ev(p, blk, 10);
+          mbar_expect_tx(&sm.q_full[st], C::kTileBytes + kTile * 4);
+          for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.q[st] + ch * C::kChunkBytes, &tmQ, &sm.q_full[st], ch * 64, r * kTile,
                         b * p.Hq + h);
-            tma_load_3d(sm.dO[st] + ch * C::kChunkBytes, &tmDO, &sm.q_full[st], ch * 64, r * kTile,
-                        b * p.Hq + h);
-          }
-          const long long row0 = static_cast<long long>(b * p.Hq + h) * p.Lq_pad + r * kTile;
           bulk_load(sm.lse2[st], p.lse2 + row0, kTile * 4, &sm.q_full[st]);
-          bulk_load(sm.delta[st], p.delta + row0, kTile * 4, &sm.q_full[st]);
-          ++qs_it;
+          if (!v_loaded) {
+            mbar_wait(&sm.v_free, (n & 1) ^ 1);
+            mbar_expect_tx(&sm.v_full, C::kTileBytes);
+            for (int ch = 0; ch < C::kChunks; ++ch)
+              tma_load_3d(sm.v + ch * C::kChunkBytes, &tmV, &sm.v_full, ch * 64, it.c * kTile,
+                          it.kb * p.Hkv + it.kh);
+            v_loaded = true;
+          }
+          const int ds_ = blk % C::kDoStages;
+          mbar_wait(&sm.do_free[ds_], ((blk / C::kDoStages) & 1) ^ 1);
+          trace_ev(p, blk, 11);
+          mbar_expect_tx(&sm.do_full[ds_], C::kTileBytes + kTile * 4);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.dO[ds_] + ch * C::kChunkBytes, &tmDO, &sm.do_full[ds_], ch * 64, r * kTile,
+                        b * p.Hq + h);
+          bulk_load(sm.delta[ds_], p.delta + row0, kTile * 4, &sm.do_full[ds_]);
+          ++blk;
+        }
+        if (!v_loaded) {  // an item with no q blocks still owns one V phase
+          mbar_wait(&sm.v_free, (n & 1) ^ 1);
+          mbar_arrive(&sm.v_full);
         }
       }
     }
@@ -285,22 +322,91 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 13) {
     if (lane == 0) {
       // ===================== MMA issuer =====================
-      constexpr uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_ts = make_idesc_bf16(128, D, 0, 1);
-      constexpr uint32_t idesc_mm = make_idesc_bf16(128, D, 1, 1);
-      constexpr uint32_t idesc_mmT = make_idesc_bf16(D, 128, 1, 1);
+      constexpr uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);   // S^T, dP^T
+      constexpr uint32_t idesc_kn = make_idesc_bf16(128, D, 0, 1);     // dV (TS), dK (SS)
+      constexpr uint32_t idesc_mm = make_idesc_bf16(128, D, 1, 1);     // dQ = dS K (D = 64)
+      constexpr uint32_t idesc_mmT = make_idesc_bf16(D, 128, 1, 1);    // dQ^T = K^T dS^T (D = 128)
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
-      int qs_it = 0;
-      uint32_t ds_ph = 0, mma2_count = 0;
-      auto mma_kmajor = [&](uint32_t d_col, uint32_t a_addr, uint32_t b_addr, uint64_t* bar) {
+      // Descriptors are rebuilt from an opaque base per GEMM (+ the K-step offset in the
+      // 14-bit address field) so ptxas does not hoist ~100 loop-invariant descriptor
+      // registers out of the persistent loop (they spill and every issue then waits on LDL).
+      auto mma_kmajor = [&](uint32_t d_col, uint32_t a_addr, uint32_t b_addr) {
+        const uint64_t a0 = make_sdesc_sw128(opaque_u32(a_addr), 16, 1024);
+        const uint64_t b0 = make_sdesc_sw128(opaque_u32(b_addr), 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kChunkBytes + (kk & 3) * 32;
-          umma_ss(tmem + d_col, make_sdesc_sw128(a_addr + off, 16, 1024),
-                  make_sdesc_sw128(b_addr + off, 16, 1024), idesc_ss, kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
+          umma_ss(tmem + d_col, a0 + off, b0 + off, idesc_ss, kk > 0 ? 1u : 0u);
         }
-        umma_commit(bar);
       };
+      auto issue_s = [&](int b) {  // S^T(b) = K Q(b)^T
+        const int st = b & 1;
+        trace_ev(p, b, 12);
+        mbar_wait(&sm.q_full[st], (b >> 1) & 1);
+        trace_ev(p, b, 13);
+        tc_fence_after();
+        mma_kmajor(kS, k_addr, smem_u32(sm.q[st]));
+        umma_commit(&sm.s_full);
+        trace_ev(p, b, 4);
+      };
+      auto issue_dp = [&](int b) {  // dP^T(b) = V dO(b)^T, after dQ(b-1) left TMEM
+        const int ds_ = b % C::kDoStages;
+        trace_ev(p, b, 14);
+        mbar_wait(&sm.do_full[ds_], (b / C::kDoStages) & 1);
+        trace_ev(p, b, 15);
+        mbar_wait(&sm.dq_empty, (b & 1) ^ 1);
+        trace_ev(p, b, 16);
+        tc_fence_after();
+        mma_kmajor(kDP, v_addr, smem_u32(sm.dO[ds_]));
+        umma_commit(&sm.dp_full);
+        trace_ev(p, b, 6);
+      };
+      auto issue_dv = [&](int b, bool acc) {  // dV += P^T(b) dO(b)   (TS)
+        const int ds_ = b % C::kDoStages;
+        trace_ev(p, b, 17);
+        mbar_wait(&sm.p_full, b & 1);
+        trace_ev(p, b, 18);
+        tc_fence_after();
+        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.dO[ds_])), C::kChunkBytes, 1024);
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          const uint32_t a_col = kS + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
+          umma_ts(tmem + kDV, tmem + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&sm.do_free[ds_]);
+      };
+      auto issue_dq = [&](int b) {  // dQ(b) over the dP columns, after dK(b) read dS^T there
+        trace_ev(p, b, 19);
+        const uint64_t k0 = make_sdesc_sw128(opaque_u32(k_addr), C::kChunkBytes, 1024);
+        const uint64_t s0 = make_sdesc_sw128(opaque_u32(ds_addr), kTile * 128, 1024);
+        if constexpr (D == 128) {
+          // dQ^T = K^T dS^T (M = head dim, N = q): the reduction warps own one head-dim
+          // index per lane and add whole 128-byte lines
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk)
+            umma_ss(tmem + kDP, k0 + kk * (2048 >> 4), s0 + kk * (2048 >> 4), idesc_mmT, kk > 0 ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk)
+            umma_ss(tmem + kDP, s0 + kk * (2048 >> 4), k0 + kk * (2048 >> 4), idesc_mm, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm.dq_full);
+        umma_commit(&sm.ds_free);
+      };
+      auto issue_dk = [&](int b, bool acc) {  // dK += dS^T(b) Q(b)   (TS: dS^T from TMEM)
+        mbar_wait(&sm.ds_full, b & 1);
+        tc_fence_after();
+        trace_ev(p, b, 5);
+        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.q[b & 1])), C::kChunkBytes, 1024);
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk) {
+          const uint32_t a_col = kDP + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
+          umma_ts(tmem + kDK, tmem + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&sm.q_free[b & 1]);
+        trace_ev(p, b, 20);
+      };
+      int blk = 0;
       for (int n = 0;; ++n) {
         const int buf = n & 1;
         mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -309,84 +415,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (item < 0) break;
         const KvItem it = decode_kv_item(p, item);
         const int T = count_tasks(p, it);
-        mbar_wait(&sm.kv_full, n & 1);
-        tc_fence_after();
-        if (T > 0) {
-          const int st0 = qs_it & 1;
-          mbar_wait(&sm.q_full[st0], (qs_it >> 1) & 1);
-          tc_fence_after();
-          mma_kmajor(kS, k_addr, smem_u32(sm.q[st0]), &sm.s_full);
-          mbar_wait(&sm.dq_free, (mma2_count & 1) ^ 1);
-          tc_fence_after();
-          mma_kmajor(kDP, v_addr, smem_u32(sm.dO[st0]), &sm.dp_full);
-          ++mma2_count;
+        mbar_wait(&sm.k_full, n & 1);
+        if (T == 0) {
+          mbar_wait(&sm.dkdv_free, (n & 1) ^ 1);
+          mbar_wait(&sm.v_full, n & 1);
+          umma_commit(&sm.dkdv_full);
+          umma_commit(&sm.k_free);
+          umma_commit(&sm.v_free);
+          continue;
         }
+        issue_s(blk);
+        mbar_wait(&sm.v_full, n & 1);
+        issue_dp(blk);
+        mbar_wait(&sm.dkdv_free, (n & 1) ^ 1);  // the previous item's dK/dV were read out
+        issue_dv(blk, false);
         for (int t = 0; t < T; ++t) {
-          const int st = (qs_it + t) & 1;
-          if (t == 0) mbar_wait(&sm.dkdv_free, (n & 1) ^ 1);  // previous item's dK/dV read out
-          mbar_wait(&sm.ds_full, ds_ph);
-          ds_ph ^= 1;
-          tc_fence_after();
-          trace_ev(p, qs_it + t, 2);
-          const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {  // MMA3: dV += P^T dO
-            const uint32_t a_col = kS + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
-            umma_ts(tmem + kDV, tmem + a_col, make_sdesc_sw128(do_addr + kk * 2048, C::kChunkBytes, 1024),
-                    idesc_ts, (t > 0 || kk > 0) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk) {  // MMA4: dK += dS^T Q
-            const uint32_t a_col = kDP + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
-            umma_ts(tmem + kDK, tmem + a_col, make_sdesc_sw128(q_addr + kk * 2048, C::kChunkBytes, 1024),
-                    idesc_ts, (t > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(&sm.q_free[st]);
-          if constexpr (D == 128) {
-            // MMA5: dQ_blk^T = K^T dS^T (M = head dim, N = q) over the dP^T columns, so the
-            // reduction warps own one head-dim index each and write coalesced 128-byte lines
-#pragma unroll
-            for (int kk = 0; kk < kTile / 16; ++kk)
-              umma_ss(tmem + kDP, make_sdesc_sw128(k_addr + kk * 2048, C::kChunkBytes, 1024),
-                      make_sdesc_sw128(ds_addr + kk * 2048, kTile * 128, 1024), idesc_mmT,
-                      kk > 0 ? 1u : 0u);
-          } else {
-#pragma unroll
-            for (int kk = 0; kk < kTile / 16; ++kk)  // MMA5: dQ_blk = dS K (over the dP^T columns)
-              umma_ss(tmem + kDP, make_sdesc_sw128(ds_addr + kk * 2048, kTile * 128, 1024),
-                      make_sdesc_sw128(k_addr + kk * 2048, C::kChunkBytes, 1024), idesc_mm,
-                      kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&sm.dq_full);
-          trace_ev(p, qs_it + t, 3);
+          const int b = blk + t;
+          if (t + 1 < T) issue_s(b + 1);
+          issue_dk(b, t > 0);
+          issue_dq(b);
+          if (t + 1 == T) umma_commit(&sm.k_free);  // K's last reader was dQ(T-1)
           if (t + 1 < T) {
-            const int st1 = (qs_it + t + 1) & 1;
-            mbar_wait(&sm.q_full[st1], ((qs_it + t + 1) >> 1) & 1);
-            tc_fence_after();
-            mma_kmajor(kS, k_addr, smem_u32(sm.q[st1]), &sm.s_full);
-            mbar_wait(&sm.dq_free, (mma2_count & 1) ^ 1);
-            tc_fence_after();
-            trace_ev(p, qs_it + t, 4);
-            mma_kmajor(kDP, v_addr, smem_u32(sm.dO[st1]), &sm.dp_full);
-            trace_ev(p, qs_it + t, 11);
-            ++mma2_count;
+            issue_dp(b + 1);
+            if (t + 2 == T) umma_commit(&sm.v_free);  // V's last reader was dP(T-1)
+            issue_dv(b + 1, true);
+          } else if (T == 1) {
+            umma_commit(&sm.v_free);
           }
         }
-        qs_it += T;
         umma_commit(&sm.dkdv_full);
-        umma_commit(&sm.kv_free);
+        blk += T;
       }
     }
     FA_BWD_TEARDOWN();
   } else if (warp < 8) {
     // ===================== compute warpgroups: P^T, dS^T =====================
-    reg_alloc<136>();
+    reg_alloc<144>();
     const int wg = warp >> 2;          // which 64 q columns
     const int wq = warp & 3;           // TMEM lane quarter
     const int j = wq * 32 + lane;      // kv row within the block
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    uint32_t s_ph = 0;
-    int qs_it = 0;
+    int blk = 0;
     for (int n = 0;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -402,78 +471,130 @@ __global__ void __launch_bounds__(kThreads, 1)
       int b, h, r;
       bool full;
       while (ti.next(b, h, r, full)) {
-        const int st = qs_it & 1;
+        const int qst = blk & 1;
+        const int ds_ = blk % C::kDoStages;
         const int q0 = r * kTile + wg * 64;
-        const auto colc = score.col(b, h, q0, kv, p.scale);
-        if (threadIdx.x == 0) trace_ev(p, qs_it, 8);
-        mbar_wait(&sm.s_full, s_ph);
-        if (threadIdx.x == 0) trace_ev(p, qs_it, 9);
-        mbar_wait(&sm.dp_full, s_ph);
-        s_ph ^= 1;
-        if (threadIdx.x == 0) trace_ev(p, qs_it, 10);
-        mbar_wait(&sm.q_full[st], (qs_it >> 1) & 1);  // lse2 / delta of this q block
+        // ---------------- phase A: P^T ----------------
+        // The preprocess stored per q column  cterm = log2(scale) - lse·log2e  (+ the q part of
+        // ALiBi), so P·scale = exp2(s·c + cterm [+ kv part of ALiBi]) is one FFMA + one MUFU.
+        // P·scale (bf16) feeds dV (rescaled by 1/scale in the epilogue) and, times mod'(s), dS.
+        mbar_wait(&sm.s_full, blk & 1);
+        mbar_wait(&sm.q_full[qst], (blk >> 1) & 1);  // cterm of this q block
         tc_fence_after();
-        if (threadIdx.x == 0) trace_ev(p, qs_it, 0);
-        uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
-        // two halves of 32 q columns keep ~100 registers live
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          const int qc = q0 + hh * 32;
-          const auto cc = colc.shifted(hh * 32);
-          uint32_t sr[32], dpr[32];
-          tmem_ld32(tm + kS + wg * 64 + hh * 32, sr);
-          tmem_ld32(tm + kDP + wg * 64 + hh * 32, dpr);
-          // mask bits for this kv row over the 32 q columns (bounds folded in)
-          const uint32_t bits = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, qc, kv, p.Lq) : 0u);
-          const float4* lse4 = reinterpret_cast<const float4*>(sm.lse2[st] + wg * 64 + hh * 32);
-          const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[st] + wg * 64 + hh * 32);
+        if (threadIdx.x == 0) trace_ev(p, blk, 0);
+        uint32_t pgp[32];  // P·scale·mod'(s) as packed bf16 pairs, kept for phase B
+        {
+          uint32_t sr[64];
+          tmem_ld32(tm + kS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(tm + kS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+          // mask bits for this kv row over the 64 q columns (bounds folded in)
+          const uint32_t bits0 = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, q0, kv, p.Lq) : 0u);
+          const uint32_t bits1 = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, q0 + 32, kv, p.Lq) : 0u);
+          const float4* ct4 = reinterpret_cast<const float4*>(sm.lse2[qst] + wg * 64);
+          const auto colc = score.col(b, h, q0, kv, p.scale);
+          float rowc = 0.f;  // ALiBi: slope·log2e·(block q start + q_offset - kv)
+          if constexpr (ScoreT::kKind == 1)
+            rowc = colc.step * static_cast<float>(r * kTile + score.p.q_offset - kv);
           tmem_wait_ld();
-          uint32_t pp[16], dsp[16];
+          uint32_t pp[32];
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 l4 = lse4[i4], d4 = dlt4[i4];
-            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-            float pv[4], dsv[4];
+          for (int i4 = 0; i4 < 16; ++i4) {
+            const float4 c4 = ct4[i4];
+            const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+            float pv[4], gv[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int ii = i4 * 4 + e;
-              float g;
-              const float x = cc.log2_grad(__uint_as_float(sr[ii]), ii, g);
-              const float pr = ((bits >> ii) & 1u) ? ex2(x - lv[e]) : 0.f;
-              pv[e] = pr;
-              dsv[e] = pr * (__uint_as_float(dpr[ii]) - dv4[e]) * (g * p.scale);
+              const float sv = __uint_as_float(sr[ii]);
+              float x;
+              if constexpr (ScoreT::kKind == 0) {
+                x = fmaf(sv, colc.c, cv[e]);
+              } else if constexpr (ScoreT::kKind == 1) {
+                x = fmaf(sv, colc.c, cv[e] + rowc);
+              } else {
+                const auto cc = colc.shifted(ii & ~31);
+                float g;
+                const float t = cc.log2_grad(sv, ii & 31, g);  // outer·tanh(u), g = 1 - tanh²
+                x = t + cv[e];
+                gv[e] = g;
+              }
+              const uint32_t bits = ii < 32 ? bits0 : bits1;
+              pv[e] = ((bits >> (ii & 31)) & 1u) ? ex2(x) : 0.f;
             }
             pp[2 * i4] = pack_bf16(pv[0], pv[1]);
             pp[2 * i4 + 1] = pack_bf16(pv[2], pv[3]);
-            dsp[2 * i4] = pack_bf16(dsv[0], dsv[1]);
-            dsp[2 * i4 + 1] = pack_bf16(dsv[2], dsv[3]);
+            if constexpr (ScoreT::kUnitGrad) {
+              pgp[2 * i4] = pp[2 * i4];
+              pgp[2 * i4 + 1] = pp[2 * i4 + 1];
+            } else {
+              pgp[2 * i4] = pack_bf16(pv[0] * gv[0], pv[1] * gv[1]);
+              pgp[2 * i4 + 1] = pack_bf16(pv[2] * gv[2], pv[3] * gv[3]);
+            }
           }
-          tmem_st16(tm + kS + wg * 64 + hh * 16, pp);    // P^T  over S^T columns already read
-          tmem_st16(tm + kDP + wg * 64 + hh * 16, dsp);  // dS^T over dP^T columns already read
-          // dS^T row j (MN-major SW128 A operand of MMA5): 16-byte units 4hh..4hh+3
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int uu = hh * 4 + u;
-            *reinterpret_cast<uint4*>(ds_row + ((uu ^ (j & 7)) << 4)) =
-                make_uint4(dsp[4 * u], dsp[4 * u + 1], dsp[4 * u + 2], dsp[4 * u + 3]);
-          }
+          tmem_st32(tm + kS + wg * 64, pp);  // P^T over S^T columns already read
         }
         tmem_wait_st();
-        fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&sm.ds_full);
-        if (threadIdx.x == 0) trace_ev(p, qs_it, 1);
-        ++qs_it;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.p_full);
+        if (threadIdx.x == 0) trace_ev(p, blk, 1);
+        // ---------------- phase B: dS^T ----------------
+        mbar_wait(&sm.dp_full, blk & 1);
+        mbar_wait(&sm.do_full[ds_], (blk / C::kDoStages) & 1);  // Δ of this q block
+        tc_fence_after();
+        if (threadIdx.x == 0) trace_ev(p, blk, 2);
+        {
+          uint32_t dpr[64];
+          tmem_ld32(tm + kDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&dpr[0]));
+          tmem_ld32(tm + kDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpr[32]));
+          const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[ds_] + wg * 64);
+          // the previous block's dQ must have read the dS^T smem buffer
+          mbar_wait(&sm.ds_free, (blk & 1) ^ 1);
+          uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
+          tmem_wait_ld();
+          uint32_t dsp[32];
+#pragma unroll
+          for (int i4 = 0; i4 < 16; ++i4) {
+            const float4 d4 = dlt4[i4];
+            const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+            float a[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int ii = i4 * 4 + e;
+              const uint32_t w = pgp[ii >> 1];
+              const float pg = __uint_as_float((ii & 1) ? (w & 0xffff0000u) : (w << 16));
+              a[e] = pg * (__uint_as_float(dpr[ii]) - dv4[e]);
+            }
+            dsp[2 * i4] = pack_bf16(a[0], a[1]);
+            dsp[2 * i4 + 1] = pack_bf16(a[2], a[3]);
+          }
+          // dS^T (bf16) over dP^T columns already read: the A operand of dK (TS)
+          tmem_st32(tm + kDP + wg * 64, dsp);
+          // dS^T row j (the MN-major operand of dQ): 16-byte units 0..7 of this warpgroup's
+          // 64-wide q chunk, 128-byte swizzle
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<uint4*>(ds_row + ((u ^ (j & 7)) << 4)) =
+                make_uint4(dsp[4 * u], dsp[4 * u + 1], dsp[4 * u + 2], dsp[4 * u + 3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.do_free[ds_]);
+        fence_proxy_async();
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ds_full);
+        if (threadIdx.x == 0) trace_ev(p, blk, 3);
+        ++blk;
       }
     }
     FA_BWD_TEARDOWN();
   } else if (warp < 12) {
     // ===================== dQ reduction + dK/dV epilogue warpgroup =====================
-    reg_alloc<152>();
+    reg_alloc<144>();
     const int wq = warp & 3;
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    uint32_t dq_ph = 0;
-    int red_it = 0;
+    int blk = 0;
     for (int n = 0;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -487,48 +608,54 @@ __global__ void __launch_bounds__(kThreads, 1)
       int T = 0, b, h, r;
       bool full;
       while (ti.next(b, h, r, full)) {
-        // dQ_blk (lanes = q rows): pull all D columns out of TMEM, release it, then reduce
-        mbar_wait(&sm.dq_full, dq_ph);
-        dq_ph ^= 1;
+        mbar_wait(&sm.dq_full, blk & 1);
         tc_fence_after();
-        if (threadIdx.x == 256) trace_ev(p, red_it, 5);
-        uint32_t a[128];
+        if (threadIdx.x == 256) trace_ev(p, blk, 7);
+        if constexpr (D == 128) {
+          // dQ^T: lane = head-dim index d = 32 wq + lane, columns = the block's 128 q rows
+          uint32_t a[128];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          tmem_ld32(tm + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&a[cc * 32]));
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&sm.dq_free);
-        if (threadIdx.x == 256) trace_ev(p, red_it, 6);
-        if (!(p.exp_flags & 1)) {
-          if constexpr (D == 128) {
-            // lanes = head-dim index d, columns = q rows of the block: per q row the warp's 32
-            // lanes add 32 consecutive floats (one 128-byte line)
-            const int d = wq * 32 + lane;
-            const int q0r = r * kTile;
-            const int nq = min(kTile, p.Lq - q0r);
-            float* base = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + q0r) * D + d;
-            if (nq == kTile) {
+          for (int cc = 0; cc < 4; ++cc)
+            tmem_ld32(tm + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&a[cc * 32]));
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.dq_empty);
+          if (threadIdx.x == 256) trace_ev(p, blk, 8);
+          // per q row the warp's 32 lanes add 32 consecutive floats: one 128-byte line per red
+          const int d = wq * 32 + lane;
+          const int nq = min(kTile, p.Lq - r * kTile);
+          float* base = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + r * kTile) * D + d;
+          if (p.exp_flags & 1) {
+          } else if (nq == kTile) {
 #pragma unroll
-              for (int qq = 0; qq < kTile; ++qq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
-            } else {
-#pragma unroll
-              for (int qq = 0; qq < kTile; ++qq)
-                if (qq < nq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
-            }
+            for (int qq = 0; qq < kTile; ++qq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
           } else {
-            const int qrow = r * kTile + wq * 32 + lane;
-            if (qrow < p.Lq) {
-              float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
 #pragma unroll
-              for (int v4 = 0; v4 < D / 4; ++v4)
-                red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
-                           __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
-            }
+            for (int qq = 0; qq < kTile; ++qq)
+              if (qq < nq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
+          }
+        } else {
+          // dQ: lane = q row 32 wq + lane, columns = the D head-dim values
+          uint32_t a[D];
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc)
+            tmem_ld32(tm + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&a[cc * 32]));
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.dq_empty);
+          const int qrow = r * kTile + wq * 32 + lane;
+          if (qrow < p.Lq) {
+            float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+#pragma unroll
+            for (int v4 = 0; v4 < D / 4; ++v4)
+              red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
+                         __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
           }
         }
-        if (threadIdx.x == 256) trace_ev(p, red_it, 7);
-        ++red_it;
+        if (threadIdx.x == 256) trace_ev(p, blk, 9);
+        ++blk;
         ++T;
       }
       // ---- epilogue: dK, dV rows (lanes = kv rows) ----
@@ -541,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int which = 0; which < 2; ++which) {
         __nv_bfloat16* dst = (which == 0 ? p.dk : p.dv) + orow * D;
         const uint32_t col = which == 0 ? kDK : kDV;
+        const float mul = which == 0 ? 1.f : 1.f / p.scale;  // dV accumulated (P·scale)^T dO
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t v[32];
@@ -555,15 +683,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
-              d4[q4] = make_uint4(pack_bf16(__uint_as_float(v[8 * q4]), __uint_as_float(v[8 * q4 + 1])),
-                                  pack_bf16(__uint_as_float(v[8 * q4 + 2]), __uint_as_float(v[8 * q4 + 3])),
-                                  pack_bf16(__uint_as_float(v[8 * q4 + 4]), __uint_as_float(v[8 * q4 + 5])),
-                                  pack_bf16(__uint_as_float(v[8 * q4 + 6]), __uint_as_float(v[8 * q4 + 7])));
+              d4[q4] = make_uint4(pack_bf16(__uint_as_float(v[8 * q4]) * mul, __uint_as_float(v[8 * q4 + 1]) * mul),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 2]) * mul, __uint_as_float(v[8 * q4 + 3]) * mul),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 4]) * mul, __uint_as_float(v[8 * q4 + 5]) * mul),
+                                  pack_bf16(__uint_as_float(v[8 * q4 + 6]) * mul, __uint_as_float(v[8 * q4 + 7]) * mul));
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm.dkdv_free);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.dkdv_free);
     }
     FA_BWD_TEARDOWN();
   } else {
@@ -572,11 +701,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef FA_BWD_TEARDOWN
 }
 
-// Δ and log2-domain lse, padded to whole q blocks (+inf lse / 0 Δ in the padding).
+// Per q row: Δ = Σ dO·O, and the column term of the compute warps' exponent,
+//   cterm = log2(scale) - lse·log2e  (+ slope·log2e·(q mod 128) for ALiBi, whose kv and
+//   block parts the compute warps add), so that exp2(s·c + cterm) = P·scale.
+// Fully masked rows (lse = -inf) and the padding to whole q blocks get cterm = -inf (P = 0).
+template <class ScoreT>
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                       const __nv_bfloat16* __restrict__ dout,
-                                      const float* __restrict__ lse, int BH, int Lq, int Lq_pad, int D,
-                                      float* __restrict__ lse2, float* __restrict__ delta) {
+                                      const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad,
+                                      int D, float scale, ScoreT score, float* __restrict__ cterm,
+                                      float* __restrict__ delta) {
   const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)BH * Lq_pad) return;
@@ -584,7 +718,7 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   const long long bh = row / Lq_pad;
   if (q >= Lq) {
     if (lane == 0) {
-      lse2[row] = INFINITY;
+      cterm[row] = -INFINITY;
       delta[row] = 0.f;
     }
     return;
@@ -601,7 +735,10 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
   if (lane == 0) {
     const float l = lse[bh * Lq + q];
-    lse2[row] = l == -INFINITY ? INFINITY : l * kLog2e;
+    float ct = l == -INFINITY ? -INFINITY : __log2f(scale) - l * kLog2e;
+    if constexpr (ScoreT::kKind == 1)
+      ct += __ldg(score.p.slopes + (int)(bh % Hq)) * kLog2e * static_cast<float>(q & (kTile - 1));
+    cterm[row] = ct;
     delta[row] = a;
   }
 }
@@ -627,9 +764,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
   FA_CHECK_CUDA(cudaMemsetAsync(dq_acc, 0, rows * D * 4, st));
-  bwd_preprocess_kernel<<<(unsigned)((prow + 7) / 8), 256, 0, st>>>(
+  bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 7) / 8), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
-      g.B * g.Hq, g.Lq, Lq_pad, D, lse2, delta);
+      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
@@ -654,7 +791,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "backward: cannot allocate the scheduler counter");
   FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
   long long* trace = nullptr;
-  if (getenv("FA_BWD_TRACE") != nullptr) {
+  if (FA_BWD_TRACE_BUILD != 0 && getenv("FA_BWD_TRACE") != nullptr) {
     FA_CHECK_CUDA(cudaMalloc(&trace, sizeof(long long) * kTraceTasks * kTraceEv));
     FA_CHECK_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * kTraceTasks * kTraceEv, st));
   }
@@ -670,35 +807,48 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
     FA_CHECK_CUDA(cudaGetLastError());
   }
   if (trace != nullptr) {  // debug: per-phase cycle deltas of CTA 0, averaged over its blocks
-    long long h[kTraceTasks * kTraceEv];
+    static long long h[kTraceTasks * kTraceEv];
     FA_CHECK_CUDA(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     FA_CHECK_CUDA(cudaStreamSynchronize(st));
     cudaFree(trace);
+    // events: 0 A start, 1 A end, 2 B start, 3 B end (compute) | 4 S issued, 5 ds_full seen
+    // (dQ issue), 6 dP issued (MMA) | 7 dq_full seen, 8 dq_empty arrived, 9 reduces issued
     double acc[12] = {0};
     int cnt = 0;
     for (int t = 1; t + 1 < kTraceTasks; ++t) {
       const long long* e = h + t * kTraceEv;
       const long long* en = h + (t + 1) * kTraceEv;
-      if (e[0] == 0 || en[0] == 0 || e[7] == 0) break;
-      acc[0] += e[1] - e[0];    // compute
-      acc[1] += e[2] - e[1];    // ds_full -> MMA sees it
-      acc[2] += e[5] - e[3];    // MMA5 issue -> dQ ready (MMA3..5 execution)
-      acc[3] += e[6] - e[5];    // dQ TMEM load
-      acc[4] += e[4] - e[6];    // dq_free -> MMA2 issue
-      acc[5] += en[0] - e[4];   // MMA2 issue -> next compute start
-      acc[6] += en[0] - e[0];   // period
-      acc[7] += e[7] - e[6];    // red issue
-      acc[8] += e[3] - e[2];    // MMA3..5 issue duration
-      acc[9] += e[11] - e[4];   // MMA2 issue duration
-      acc[10] += en[9] - e[11]; // MMA2 issued -> next s_full seen
-      acc[11] += en[10] - en[9];// s_full -> dp_full
+      if (e[0] == 0 || en[0] == 0 || e[9] == 0 || en[6] == 0) break;
+      acc[0] += e[1] - e[0];    // phase A
+      acc[1] += e[2] - e[1];    // wait for dP
+      acc[2] += e[3] - e[2];    // phase B
+      acc[3] += en[0] - e[3];   // B end -> next A start
+      acc[4] += e[5] - e[3];    // ds_full -> MMA sees it
+      acc[5] += e[7] - e[5];    // dQ issue -> reduce sees dq_full
+      acc[6] += e[8] - e[7];    // dQ TMEM drain
+      acc[7] += en[6] - e[8];   // dq_empty -> next dP issued
+      acc[8] += en[2] - en[6];  // dP issued -> next B start
+      acc[9] += en[0] - e[0];   // period
+      acc[10] += en[4] - en[10];  // Q load issued -> S issued (includes the q_full wait)
+      acc[11] += en[6] - en[11];  // dO load issued -> dP issued
       ++cnt;
+    }
+    if (getenv("FA_BWD_TRACE")[0] == '2') {
+      static const char* names[24] = {"A0", "A1", "B0", "B1", "Sdone", "dQiss", "dPiss", "rdq", "rempty", "rred",
+                                      "ldQ", "ldO", "S_in", "S_q", "dP_in", "dP_do", "dP_em", "dV_in", "dV_p",
+                                      "dQ_in", "dKiss", "", "", ""};
+      const long long t0 = h[10 * kTraceEv + 0];
+      for (int t = 10; t < 14; ++t) {
+        fprintf(stderr, "[bwd trace] block %d:", t);
+        for (int e = 0; e < 21; ++e)
+          if (h[t * kTraceEv + e] != 0) fprintf(stderr, " %s=%lld", names[e], h[t * kTraceEv + e] - t0);
+        fprintf(stderr, "\n");
+      }
     }
     if (cnt > 0)
       fprintf(stderr,
-              "[bwd trace] blocks=%d cycles: compute %.0f | ds->mma %.0f | mma3-5 %.0f | dq ld %.0f | "
-              "free->mma2 %.0f | mma2->compute %.0f | period %.0f | red issue %.0f | mma3-5 issue %.0f | "
-              "mma2 issue %.0f | mma2 issued->s_full %.0f | s_full->dp_full %.0f\n",
+              "[bwd trace] blocks=%d cycles: A %.0f | wait dP %.0f | B %.0f | B->nextA %.0f | ds->mma %.0f | "
+              "dQ mma %.0f | dQ drain %.0f | empty->dP %.0f | dP->B %.0f | period %.0f | Qld->S %.0f | dOld->dP %.0f\n",
               cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
               acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, acc[9] / cnt, acc[10] / cnt, acc[11] / cnt);
   }

@@ -183,6 +183,8 @@ template <int K, bool Precise = false>
 struct ScoreFn {
   ScoreParams p;
   static constexpr bool kIdentity = (K == 0);
+  static constexpr int kKind = K;
+  static constexpr bool kUnitGrad = (K & kScoreSoftCap) == 0;  // d apply / d s == 1
   __device__ __forceinline__ float apply(float s, int b, int h, int q, int kv) const {
     (void)b;
     if constexpr (K & kScoreAlibi) {  // alibi, mask_library.cpp:61-63 (slope of q-head h)

@@ -48,6 +48,8 @@
 namespace fa {
 
 CUresult encode_tile_map(CUtensorMap* map, const void* base, int bh, int len, int d);
+CUresult encode_f32_map(CUtensorMap* map, const void* base, int bh, int len, int d, int box_d,
+                        int box_rows);
 int* scheduler_counter(int slot);
 
 namespace {
@@ -91,12 +93,20 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
   }
 }
 
+#ifndef FA_BWD_DQ_TMA
+#define FA_BWD_DQ_TMA 1
+#endif
 template <int D>
 struct BCfg {
   static constexpr int kChunks = D / 64;
   static constexpr int kTileBytes = kTile * D * 2;
   static constexpr int kChunkBytes = kTile * 128;
-  static constexpr int kDoStages = 2;
+  // dQ goes to L2 by TMA reduce-add from per-warp smem staging tiles (kTmaReduce) or by
+  // red.global.add from registers; at D = 128 the staging costs one dO stage (227 KB budget)
+  static constexpr bool kTmaReduce = FA_BWD_DQ_TMA != 0;
+  static constexpr int kDoStages = (kTmaReduce && D == 128) ? 1 : 2;
+  static constexpr int kBoxD = D == 128 ? 32 : 64;                     // staging tile: 32 q x kBoxD
+  static constexpr int kStageFloats = kTmaReduce ? 32 * kBoxD : 4;
 };
 
 template <int D>
@@ -108,6 +118,7 @@ struct alignas(1024) BSmem {
   uint8_t ds[kTile * kTile * 2];  // dS^T [kv][q], SW128, two 64-wide q chunks
   float lse2[2][kTile];
   float delta[BCfg<D>::kDoStages][kTile];
+  float dq_stage[4][2][BCfg<D>::kStageFloats];  // per reduction warp, double-buffered
   uint64_t k_full, v_full, k_free, v_free;
   uint64_t q_full[2], q_free[2];
   uint64_t do_full[BCfg<D>::kDoStages], do_free[BCfg<D>::kDoStages];
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV,
                           const __grid_constant__ CUtensorMap tmDO,
-                          const BwdParams p, MaskT mask,
+                          const __grid_constant__ CUtensorMap tmDQ, const BwdParams p, MaskT mask,
                           ScoreT score) {
   using C = BCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -234,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
+    if constexpr (C::kTmaReduce) tma_prefetch_desc(&tmDQ);
   }
   if (warp == 13) {
     tmem_alloc(&sm.tmem_base, 512);
@@ -594,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     reg_alloc<144>();
     const int wq = warp & 3;
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    int blk = 0;
+    int blk = 0, stage_it = 0;
     for (int n = 0;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -622,6 +634,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.dq_empty);
           if (threadIdx.x == 256) trace_ev(p, blk, 8);
+          if constexpr (C::kTmaReduce) {
+            // four 32 (q) x 32 (d) fp32 tiles per warp: st.shared rows of 128 B (lane = d),
+            // then one TMA reduce-add each (rows past Q_LEN are clipped by the tensor map)
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4, ++stage_it) {
+              float* stg = sm.dq_stage[wq][stage_it & 1];
+              if (lane == 0) bulk_wait_group_read<1>();  // the reduce that last read this buffer
+              __syncwarp();
+#pragma unroll
+              for (int qq = 0; qq < 32; ++qq) stg[qq * 32 + lane] = __uint_as_float(a[c4 * 32 + qq]);
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0 && !(p.exp_flags & 1)) {
+                tma_reduce_add_3d(&tmDQ, stg, wq * 32, r * kTile + c4 * 32, b * p.Hq + h);
+                bulk_commit_group();
+              }
+            }
+          } else {
           // per q row the warp's 32 lanes add 32 consecutive floats: one 128-byte line per red
           const int d = wq * 32 + lane;
           const int nq = min(kTile, p.Lq - r * kTile);
@@ -635,6 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int qq = 0; qq < kTile; ++qq)
               if (qq < nq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
           }
+          }
         } else {
           // dQ: lane = q row 32 wq + lane, columns = the D head-dim values
           uint32_t a[D];
@@ -645,13 +676,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.dq_empty);
-          const int qrow = r * kTile + wq * 32 + lane;
-          if (qrow < p.Lq) {
-            float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+          if constexpr (C::kTmaReduce) {
+            // one 32 (q) x D fp32 tile per warp (row per lane; bank conflicts accepted at D=64)
+            float* stg = sm.dq_stage[wq][stage_it & 1];
+            if (lane == 0) bulk_wait_group_read<1>();
+            __syncwarp();
 #pragma unroll
-            for (int v4 = 0; v4 < D / 4; ++v4)
-              red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
-                         __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
+            for (int u = 0; u < D / 4; ++u) {
+              float4 w4;
+              w4.x = __uint_as_float(a[4 * u]);
+              w4.y = __uint_as_float(a[4 * u + 1]);
+              w4.z = __uint_as_float(a[4 * u + 2]);
+              w4.w = __uint_as_float(a[4 * u + 3]);
+              *reinterpret_cast<float4*>(stg + lane * D + 4 * u) = w4;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && !(p.exp_flags & 1)) {
+              tma_reduce_add_3d(&tmDQ, stg, 0, r * kTile + wq * 32, b * p.Hq + h);
+              bulk_commit_group();
+            }
+            ++stage_it;
+          } else {
+            const int qrow = r * kTile + wq * 32 + lane;
+            if (qrow < p.Lq) {
+              float* dst = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + qrow) * D;
+#pragma unroll
+              for (int v4 = 0; v4 < D / 4; ++v4)
+                red_add_v4(dst + v4 * 4, __uint_as_float(a[4 * v4]), __uint_as_float(a[4 * v4 + 1]),
+                           __uint_as_float(a[4 * v4 + 2]), __uint_as_float(a[4 * v4 + 3]));
+            }
           }
         }
         if (threadIdx.x == 256) trace_ev(p, blk, 9);
@@ -693,6 +747,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.dkdv_free);
+    }
+    if constexpr (C::kTmaReduce) {
+      if (lane == 0) bulk_wait_group<0>();  // every dQ reduce-add has landed before exit
+      __syncwarp();
     }
     FA_BWD_TEARDOWN();
   } else {
@@ -770,12 +828,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
-  CUtensorMap mq, mk, mv, mdo;
+  CUtensorMap mq, mk, mv, mdo, mdq;
   CUresult cr;
   if ((cr = encode_tile_map(&mq, q, g.B * g.Hq, g.Lq, D)) != CUDA_SUCCESS ||
       (cr = encode_tile_map(&mk, k, g.Bkv * g.Hkv, g.Lkv, D)) != CUDA_SUCCESS ||
       (cr = encode_tile_map(&mv, v, g.Bkv * g.Hkv, g.Lkv, D)) != CUDA_SUCCESS ||
-      (cr = encode_tile_map(&mdo, dout, g.B * g.Hq, g.Lq, D)) != CUDA_SUCCESS)
+      (cr = encode_tile_map(&mdo, dout, g.B * g.Hq, g.Lq, D)) != CUDA_SUCCESS ||
+      (cr = encode_f32_map(&mdq, dq_acc, g.B * g.Hq, g.Lq, D, BCfg<D>::kBoxD, 32)) != CUDA_SUCCESS)
     return set_error(FA_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")");
   BwdParams p{};
   p.B = g.B; p.Hq = g.Hq; p.Hkv = g.Hkv; p.Bkv = g.Bkv; p.Lq = g.Lq; p.Lkv = g.Lkv; p.G = g.G;
@@ -802,7 +861,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
   if (grid > 0) {
-    kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, mdo, p, mask, score);
+    kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, mdo, mdq, p, mask, score);
     count_launch();
     FA_CHECK_CUDA(cudaGetLastError());
   }

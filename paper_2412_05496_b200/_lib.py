@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflexattn_b200.so")
+# FA_LIB_PATH: developer override (e.g. an instrumented build); the product path is in-tree
+LIB_PATH = os.environ.get("FA_LIB_PATH") or os.path.join(HERE, "libflexattn_b200.so")
 
 FA_F32, FA_BF16 = 0, 1
 

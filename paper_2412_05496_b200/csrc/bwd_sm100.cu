@@ -40,6 +40,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "internal.h"
 #include "mods.cuh"
@@ -500,8 +501,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tm + kS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
           tmem_ld32(tm + kS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           // mask bits for this kv row over the 64 q columns (bounds folded in)
-          const uint32_t bits0 = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, q0, kv, p.Lq) : 0u);
-          const uint32_t bits1 = full ? 0xffffffffu : (kv_in ? mask.bits32_q(b, h, q0 + 32, kv, p.Lq) : 0u);
+          uint32_t bits0 = 0u, bits1 = 0u;
+          if (!full && kv_in) {
+            bits0 = mask.bits32_q(b, h, q0, kv, p.Lq);
+            bits1 = mask.bits32_q(b, h, q0 + 32, kv, p.Lq);
+          }
           const float4* ct4 = reinterpret_cast<const float4*>(sm.lse2[qst] + wg * 64);
           const auto colc = score.col(b, h, q0, kv, p.scale);
           float rowc = 0.f;  // ALiBi: slope·log2e·(block q start + q_offset - kv)
@@ -509,40 +513,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             rowc = colc.step * static_cast<float>(r * kTile + score.p.q_offset - kv);
           tmem_wait_ld();
           uint32_t pp[32];
+          // full blocks skip mask_mod entirely (no per-score select)
+          auto body = [&](auto masked) {
 #pragma unroll
-          for (int i4 = 0; i4 < 16; ++i4) {
-            const float4 c4 = ct4[i4];
-            const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-            float pv[4], gv[4];
+            for (int i4 = 0; i4 < 16; ++i4) {
+              const float4 c4 = ct4[i4];
+              const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+              float pv[4], gv[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int ii = i4 * 4 + e;
-              const float sv = __uint_as_float(sr[ii]);
-              float x;
-              if constexpr (ScoreT::kKind == 0) {
-                x = fmaf(sv, colc.c, cv[e]);
-              } else if constexpr (ScoreT::kKind == 1) {
-                x = fmaf(sv, colc.c, cv[e] + rowc);
-              } else {
-                const auto cc = colc.shifted(ii & ~31);
-                float g;
-                const float t = cc.log2_grad(sv, ii & 31, g);  // outer·tanh(u), g = 1 - tanh²
-                x = t + cv[e];
-                gv[e] = g;
+              for (int e = 0; e < 4; ++e) {
+                const int ii = i4 * 4 + e;
+                const float sv = __uint_as_float(sr[ii]);
+                float x;
+                if constexpr (ScoreT::kKind == 0) {
+                  x = fmaf(sv, colc.c, cv[e]);
+                } else if constexpr (ScoreT::kKind == 1) {
+                  x = fmaf(sv, colc.c, cv[e] + rowc);
+                } else {
+                  const auto cc = colc.shifted(ii & ~31);
+                  float g;
+                  const float t = cc.log2_grad(sv, ii & 31, g);  // outer·tanh(u), g = 1 - tanh²
+                  x = t + cv[e];
+                  gv[e] = g;
+                }
+                if constexpr (decltype(masked)::value) {
+                  const uint32_t bits = ii < 32 ? bits0 : bits1;
+                  pv[e] = ((bits >> (ii & 31)) & 1u) ? ex2(x) : 0.f;
+                } else {
+                  pv[e] = ex2(x);
+                }
               }
-              const uint32_t bits = ii < 32 ? bits0 : bits1;
-              pv[e] = ((bits >> (ii & 31)) & 1u) ? ex2(x) : 0.f;
+              pp[2 * i4] = pack_bf16(pv[0], pv[1]);
+              pp[2 * i4 + 1] = pack_bf16(pv[2], pv[3]);
+              if constexpr (ScoreT::kUnitGrad) {
+                pgp[2 * i4] = pp[2 * i4];
+                pgp[2 * i4 + 1] = pp[2 * i4 + 1];
+              } else {
+                pgp[2 * i4] = pack_bf16(pv[0] * gv[0], pv[1] * gv[1]);
+                pgp[2 * i4 + 1] = pack_bf16(pv[2] * gv[2], pv[3] * gv[3]);
+              }
             }
-            pp[2 * i4] = pack_bf16(pv[0], pv[1]);
-            pp[2 * i4 + 1] = pack_bf16(pv[2], pv[3]);
-            if constexpr (ScoreT::kUnitGrad) {
-              pgp[2 * i4] = pp[2 * i4];
-              pgp[2 * i4 + 1] = pp[2 * i4 + 1];
-            } else {
-              pgp[2 * i4] = pack_bf16(pv[0] * gv[0], pv[1] * gv[1]);
-              pgp[2 * i4 + 1] = pack_bf16(pv[2] * gv[2], pv[3] * gv[3]);
-            }
-          }
+          };
+          if (full) body(std::false_type{});
+          else body(std::true_type{});
           tmem_st32(tm + kS + wg * 64, pp);  // P^T over S^T columns already read
         }
         tmem_wait_st();

@@ -587,6 +587,21 @@ CUresult encode_tile_map(CUtensorMap* map, const void* base, int bh, int len, in
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
+// 3-D map over a (BH, L, D) bf16 tensor with a (64, box_rows, 1) box and 128-byte swizzle:
+// the target of TMA stores of output rows staged in swizzled shared memory.
+CUresult encode_store_map(CUtensorMap* map, const void* base, int bh, int len, int d, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (enc == nullptr) return CUDA_ERROR_NOT_SUPPORTED;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(len),
+                        static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, static_cast<cuuint64_t>(len) * d * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
 // 3-D map over a (BH, L, D) fp32 tensor with a (box_d, box_rows, 1) box and no swizzle: the
 // target of the backward's TMA reduce-add of dQ (rows past L are clipped per head).
 CUresult encode_f32_map(CUtensorMap* map, const void* base, int bh, int len, int d, int box_d,

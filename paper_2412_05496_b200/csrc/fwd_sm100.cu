@@ -28,8 +28,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "internal.h"
 #include "mods.cuh"
@@ -50,7 +53,7 @@ int* scheduler_counter(int slot) {
 
 namespace {
 
-constexpr int kThreads = 320;  // 8 softmax warps + producer + MMA; <= 200 regs/thread
+constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, 2 idle) warpgroup
 constexpr int kTile = 128;           // query rows per tile == kv rows per block
 constexpr int kMaxCols = 1024;       // max kv blocks per row (KV_LEN <= 131072)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -68,7 +71,23 @@ struct FwdParams {
   float scale, scale_log2;
   int npairs, num_items;
   int* work_counter;  // zeroed before launch; dynamic item scheduler
+  long long* trace;   // debug only (FA_FWD_TRACE with an instrumented build)
 };
+
+// Compiled in only with -DFA_FWD_TRACE_BUILD=1. Slots [tile-step][event] of CTA 0.
+#ifndef FA_FWD_TRACE_BUILD
+#define FA_FWD_TRACE_BUILD 0
+#endif
+constexpr int kFTraceSteps = 512, kFTraceEv = 8;
+__device__ __forceinline__ void ftrace(const FwdParams& p, int step, int ev) {
+  if constexpr (FA_FWD_TRACE_BUILD != 0) {
+    if (p.trace != nullptr && blockIdx.x == 0 && step < kFTraceSteps) {
+      long long t;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+      p.trace[step * kFTraceEv + ev] = t;
+    }
+  }
+}
 
 template <int D>
 struct Cfg {
@@ -152,7 +171,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
+  // Each role ends in its own copy of the teardown so no code is shared between warpgroups
+  // with different setmaxnreg budgets (ptxas allocates registers per region).
+#define FA_FWD_TEARDOWN()  \
+  do {                     \
+    tc_fence_before();     \
+    __syncthreads();       \
+    if (warp == 9) {       \
+      tc_fence_after();    \
+      tmem_dealloc(tmem, 512); \
+    }                      \
+    return;                \
+  } while (0)
   if (warp >= 8) {
+    reg_dealloc<56>();
     if (warp == 8 && lane == 0) {
       // ===================== TMA producer =====================
       int kv_it = 0;
@@ -228,27 +260,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
       const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
       uint32_t p_phase[2] = {0, 0};
+      int mg[2] = {0, 0};  // per-tile step counters (trace only)
       int kv_it = 0;
       int n = 0;
+      // descriptors rebuilt per GEMM from an opaque base (+ K-step offsets in the address
+      // field): ptxas would otherwise hoist them all out of the loop and spill
       auto issue_qk = [&](int t, int st) {
-        const uint32_t kaddr = smem_u32(sm.k[st]);
+        const uint64_t a0 = make_sdesc_sw128(opaque_u32(q_addr[t]), 16, 1024);
+        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.k[st])), 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kChunkBytes + (kk & 3) * 32;
-          const uint64_t ad = make_sdesc_sw128(q_addr[t] + off, 16, 1024);
-          const uint64_t bd = make_sdesc_sw128(kaddr + off, 16, 1024);
-          umma_ss(tmem + t * 128, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
+          umma_ss(tmem + t * 128, a0 + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&sm.s_full[t]);
       };
       auto issue_pv = [&](int t, int st, bool acc) {
-        const uint32_t vaddr = smem_u32(sm.v[st]);
+        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.v[st])), C::kChunkBytes, 1024);
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk) {
-          const uint64_t bd = make_sdesc_sw128(vaddr + kk * 2048, C::kChunkBytes, 1024);
-          umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, bd, idesc_pv,
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
                   (acc || kk > 0) ? 1u : 0u);
-        }
       };
       for (;; ++n) {
         const int buf = n & 1;
@@ -293,8 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_wait(&sm.p_full[t], p_phase[t]);
               p_phase[t] ^= 1;
               tc_fence_after();
+              ftrace(p, mg[t], 4 + t);
               issue_pv(t, st, !first_pv[t]);
               first_pv[t] = false;
+              ++mg[t];
             }
             if (en & in_bit) {
               if (!k1_ready) {
@@ -303,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 k1_ready = true;
               }
               issue_qk(t, st1);
+              ftrace(p, mg[t], 6 + t);
               if (last_qk[t] == j + 1) umma_commit(&sm.q_free[t]);
             }
           }
@@ -313,8 +348,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sm.item_empty[buf]);
       }
     }
+    FA_FWD_TEARDOWN();
   } else {
     // ===================== softmax / correction / epilogue =====================
+    reg_alloc<224>();
     const int t = warp >> 2;               // tile
     const int wq = warp & 3;               // TMEM lane quarter
     const int row = wq * 32 + lane;        // query row within the tile
@@ -324,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t in_bit = t == 0 ? kIn0 : kIn1;
     const uint32_t full_bit = t == 0 ? kFull0 : kFull1;
     uint32_t s_phase = 0;
-    int n = 0;
+    int n = 0, gs = 0;
     for (;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -344,47 +381,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.s_full[t], s_phase);
         s_phase ^= 1;
         tc_fence_after();
-        // pass 1: score_mod in the log2 domain (+ mask_mod and bounds in partial blocks),
-        // row max. A plain (identity) score keeps raw scores and scales the max once.
+        if (row == 0) ftrace(p, gs, t * 2 + 0);
+        // One TMEM read of the whole 128-score row into registers: score_mod in the log2
+        // domain (+ mask_mod and bounds in partial blocks) and the row max, then the
+        // exponentials straight from registers. A plain (identity) score keeps raw scores
+        // and scales the max once (c > 0 commutes with max).
         constexpr bool kPlain = ScoreT::kIdentity;
         const auto rowc = score.row(it.b, it.h, qi, kv0, p.scale);
-        float mx = -INFINITY;
-#pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-          const int kvc = kv0 + cc * 32;
-          const auto rc = rowc.shifted(cc * 32);
-          uint32_t r[32];
-          tmem_ld32(s_tm + cc * 32, r);
-          if (full) {
-            tmem_wait_ld();
-            if constexpr (kPlain) {
+        uint32_t r[128];
 #pragma unroll
-              for (int i = 0; i < 32; i += 2)
-                mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
-            } else {
+        for (int cc = 0; cc < 4; ++cc)
+          tmem_ld32(s_tm + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[cc * 32]));
+        uint32_t bits[4] = {~0u, ~0u, ~0u, ~0u};
+        if (!full) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float v = rc.log2(__uint_as_float(r[i]), i);
-                r[i] = __float_as_uint(v);
-                mx = fmaxf(mx, v);
-              }
-              tmem_st32(s_tm + cc * 32, r);
-            }
-          } else {
-            const uint32_t bits = qi < p.Lq ? mask.bits32(it.b, it.h, qi, kvc, p.Lkv) : 0u;
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float v = kPlain ? __uint_as_float(r[i]) : rc.log2(__uint_as_float(r[i]), i);
-              v = ((bits >> i) & 1u) ? v : -INFINITY;
-              r[i] = __float_as_uint(v);
-              mx = fmaxf(mx, v);
-            }
-            tmem_st32(s_tm + cc * 32, r);
-          }
+          for (int cc = 0; cc < 4; ++cc)
+            bits[cc] = qi < p.Lq ? mask.bits32(it.b, it.h, qi, kv0 + cc * 32, p.Lkv) : 0u;
         }
-        if (!(kPlain && full)) tmem_wait_st();
-        if constexpr (kPlain) mx *= rowc.c;  // c > 0: max commutes with the scale
+        tmem_wait_ld();
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        auto pass1 = [&](auto masked) {
+#pragma unroll
+          for (int i = 0; i < 128; i += 2) {
+            float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
+            if constexpr (!kPlain) {
+              const auto rc = rowc.shifted(i & ~31);
+              v0 = rc.log2(v0, i & 31);
+              v1 = rc.log2(v1, (i + 1) & 31);
+            }
+            if constexpr (decltype(masked)::value) {
+              v0 = ((bits[i >> 5] >> (i & 31)) & 1u) ? v0 : -INFINITY;
+              v1 = ((bits[i >> 5] >> ((i + 1) & 31)) & 1u) ? v1 : -INFINITY;
+            }
+            if constexpr (!kPlain || decltype(masked)::value) {
+              r[i] = __float_as_uint(v0);
+              r[i + 1] = __float_as_uint(v1);
+            }
+            mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], v0, v1);
+          }
+        };
+        if (full) pass1(std::false_type{});
+        else pass1(std::true_type{});
+        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        if constexpr (kPlain) mx *= rowc.c;
         // lazy rescale (warp-uniform decision; tcgen05.ld/st are warp-collective)
         const float m_new = fmaxf(m, mx);
         const bool need = (m != -INFINITY) && (m_new > m + kRescaleThreshold);
@@ -392,42 +431,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float alpha = need ? ex2(m - m_new) : 1.f;
 #pragma unroll 1
           for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t r[32];
-            tmem_ld32(o_tm + cc * 32, r);
+            uint32_t o[32];
+            tmem_ld32(o_tm + cc * 32, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(o_tm + cc * 32, r);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(o_tm + cc * 32, o);
           }
           l *= alpha;
         }
         if (need || m == -INFINITY) m = m_new;
         const float msub = (m == -INFINITY) ? 0.f : m;
-        // pass 2: P = exp2(x - m) as packed bf16 into S's first 64 columns (64 scores per step)
-        const float xs = kPlain ? rowc.c : 1.f;
-        float lsum = 0.f;
+        // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1)
+        const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
+        const float2 nm2 = make_float2(-msub, -msub);
+        float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+        uint32_t pk[64];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          uint32_t a[32], b2[32], r[32];
-          tmem_ld32(s_tm + cc * 64, a);
-          tmem_ld32(s_tm + cc * 64 + 32, b2);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = ex2(fmaf(__uint_as_float(a[2 * i]), xs, -msub));
-            const float p1 = ex2(fmaf(__uint_as_float(a[2 * i + 1]), xs, -msub));
-            const float p2 = ex2(fmaf(__uint_as_float(b2[2 * i]), xs, -msub));
-            const float p3 = ex2(fmaf(__uint_as_float(b2[2 * i + 1]), xs, -msub));
-            lsum += (p0 + p1) + (p2 + p3);
-            r[i] = pack_bf16(p0, p1);
-            r[16 + i] = pack_bf16(p2, p3);
-          }
-          tmem_st32(s_tm + cc * 32, r);
+        for (int i = 0; i < 64; ++i) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                      xs2, nm2);
+          const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+          ls[i & 3] = __fadd2_rn(ls[i & 3], pv);
+          pk[i] = pack_bf16(pv.x, pv.y);
         }
-        l += lsum;
+        tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        const float2 l01 = __fadd2_rn(ls[0], ls[1]), l23 = __fadd2_rn(ls[2], ls[3]);
+        const float2 lt = __fadd2_rn(l01, l23);
+        l += lt.x + lt.y;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&sm.p_full[t]);
+        if (row == 0) ftrace(p, gs, t * 2 + 1);
+        ++gs;
       }
       // ---- epilogue: O / l -> bf16, lse ----
       mbar_wait(&sm.o_full[t], n & 1);
@@ -467,14 +505,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
     }
+    FA_FWD_TEARDOWN();
   }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
+#undef FA_FWD_TEARDOWN
 }
 
 // ---------------------------------------------------------------- host side
@@ -534,6 +567,12 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   p.npairs = (g.rows + 1) / 2;
   p.num_items = g.B * g.Hq * p.npairs;
   p.work_counter = scheduler_counter(0);
+  long long* trace = nullptr;
+  if (FA_FWD_TRACE_BUILD != 0 && getenv("FA_FWD_TRACE") != nullptr) {
+    FA_CHECK_CUDA(cudaMalloc(&trace, sizeof(long long) * kFTraceSteps * kFTraceEv));
+    FA_CHECK_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * kFTraceSteps * kFTraceEv, st));
+  }
+  p.trace = trace;
   FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "forward: cannot allocate the scheduler counter");
   FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
   const size_t smem = sizeof(Smem<D>) + 1024;
@@ -544,6 +583,29 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, p, mask, score);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
+  if (trace != nullptr) {  // debug: per-step events of CTA 0 (tile 0 and 1)
+    static long long h[kFTraceSteps * kFTraceEv];
+    FA_CHECK_CUDA(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FA_CHECK_CUDA(cudaStreamSynchronize(st));
+    cudaFree(trace);
+    const long long t0 = h[20 * kFTraceEv];
+    for (int s = 20; s < 28; ++s) {
+      const long long* e = h + s * kFTraceEv;
+      fprintf(stderr, "[fwd trace] step %d: S0seen %lld P0done %lld PV0 %lld QK0next %lld | S1seen %lld P1done %lld PV1 %lld QK1next %lld\n",
+              s, e[0] - t0, e[1] - t0, e[4] - t0, e[6] - t0, e[2] - t0, e[3] - t0, e[5] - t0, e[7] - t0);
+    }
+    double sm0 = 0, per = 0;
+    int cnt = 0;
+    for (int s = 1; s + 1 < kFTraceSteps; ++s) {
+      const long long* e = h + s * kFTraceEv;
+      const long long* en = h + (s + 1) * kFTraceEv;
+      if (e[0] == 0 || e[1] == 0 || en[0] == 0) break;
+      sm0 += e[1] - e[0];
+      per += en[0] - e[0];
+      ++cnt;
+    }
+    if (cnt) fprintf(stderr, "[fwd trace] steps=%d softmax0 %.0f cycles, tile-0 period %.0f cycles\n", cnt, sm0 / cnt, per / cnt);
+  }
   return FA_OK;
 }
 

@@ -53,6 +53,9 @@ int* scheduler_counter(int slot) {
 
 namespace {
 
+#ifndef FA_FWD_EMU
+#define FA_FWD_EMU 1  // part of the exponentials on the FMA pipe in full blocks
+#endif
 constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, 2 idle) warpgroup
 constexpr int kTile = 128;           // query rows per tile == kv rows per block
 constexpr int kMaxCols = 1024;       // max kv blocks per row (KV_LEN <= 131072)
@@ -107,7 +110,7 @@ struct alignas(1024) Smem {
   int32_t uitem[2];   // work item of the buffer, -1 = no more work
   uint64_t q_full[2], q_free[2];
   uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages], kv_empty[Cfg<D>::kStages];
-  uint64_t s_full[2], p_full[2], o_full[2];
+  uint64_t s_full[2], p_full[2][2], o_full[2];  // p_full[tile][half of the kv block]
   uint64_t item_full[2], item_empty[2];
   uint32_t tmem_base;
 };
@@ -145,7 +148,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_full[t], 1);
       mbar_init(&sm.q_free[t], 1);
       mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], 128);
+      // split P (soft-capped scores): one arrival per warp and half; else per thread, [1] only
+      mbar_init(&sm.p_full[t][0], ScoreT::kUnitGrad ? 128 : 4);
+      mbar_init(&sm.p_full[t][1], ScoreT::kUnitGrad ? 128 : 4);
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
@@ -275,12 +280,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&sm.s_full[t]);
       };
-      auto issue_pv = [&](int t, int st, bool acc) {
+      // O_t += P_t V: the first 64 kv (P columns 0-31) as soon as the softmax released them,
+      // the rest when the second half of P is in TMEM
+      constexpr bool kSplitP = !ScoreT::kUnitGrad;  // see the softmax
+      auto issue_pv = [&](int t, int st, bool acc, uint32_t ph) {
         const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.v[st])), C::kChunkBytes, 1024);
+        if constexpr (kSplitP) {
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
-                  (acc || kk > 0) ? 1u : 0u);
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait(&sm.p_full[t][hf], ph);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = hf * 4; kk < hf * 4 + 4; ++kk)
+              umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
+                      (acc || kk > 0) ? 1u : 0u);
+          }
+        } else {
+          mbar_wait(&sm.p_full[t][1], ph);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk)
+            umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
+                    (acc || kk > 0) ? 1u : 0u);
+        }
       };
       for (;; ++n) {
         const int buf = n & 1;
@@ -322,11 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t = 0; t < 2; ++t) {
             const uint32_t in_bit = t == 0 ? kIn0 : kIn1;
             if (e & in_bit) {
-              mbar_wait(&sm.p_full[t], p_phase[t]);
-              p_phase[t] ^= 1;
-              tc_fence_after();
               ftrace(p, mg[t], 4 + t);
-              issue_pv(t, st, !first_pv[t]);
+              issue_pv(t, st, !first_pv[t], p_phase[t]);
+              p_phase[t] ^= 1;
               first_pv[t] = false;
               ++mg[t];
             }
@@ -442,28 +462,61 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (need || m == -INFINITY) m = m_new;
         const float msub = (m == -INFINITY) ? 0.f : m;
-        // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1)
+        // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1).
+        // With a soft-capped score (tanh + exp2 per score: the MUFU is the bottleneck) each half
+        // releases its PV MMAs on its own (p_full[t][half]) and, in full blocks, a quarter of
+        // the exponentials run on the FMA pipe (exp2_poly2); measured slower for the others.
+        constexpr bool kSplitP = !ScoreT::kUnitGrad;
         const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
         const float2 nm2 = make_float2(-msub, -msub);
         float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
-        uint32_t pk[64];
+        if constexpr (kSplitP) {
+          auto exp_half = [&](int hf, auto emulate) {
+            uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
-                                      xs2, nm2);
-          const float2 pv = make_float2(ex2(x.x), ex2(x.y));
-          ls[i & 3] = __fadd2_rn(ls[i & 3], pv);
-          pk[i] = pack_bf16(pv.x, pv.y);
+            for (int k = 0; k < 32; ++k) {
+              const int i = hf * 32 + k;
+              const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                          xs2, nm2);
+              float2 pv;
+              if (decltype(emulate)::value && FA_FWD_EMU != 0 && (k & 3) == 3) pv = exp2_poly2(x);
+              else pv = make_float2(ex2(x.x), ex2(x.y));
+              ls[k & 3] = __fadd2_rn(ls[k & 3], pv);
+              pk[k] = pack_bf16(pv.x, pv.y);
+            }
+            tmem_st32(s_tm + hf * 32, pk);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full[t][hf]);
+          };
+          if (full) {
+            exp_half(0, std::true_type{});
+            exp_half(1, std::true_type{});
+          } else {
+            exp_half(0, std::false_type{});
+            exp_half(1, std::false_type{});
+          }
+        } else {
+          uint32_t pk[64];
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                        xs2, nm2);
+            const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+            ls[i & 3] = __fadd2_rn(ls[i & 3], pv);
+            pk[i] = pack_bf16(pv.x, pv.y);
+          }
+          tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+          tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.p_full[t][1]);
         }
-        tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
         const float2 l01 = __fadd2_rn(ls[0], ls[1]), l23 = __fadd2_rn(ls[2], ls[3]);
         const float2 lt = __fadd2_rn(l01, l23);
         l += lt.x + lt.y;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&sm.p_full[t]);
         if (row == 0) ftrace(p, gs, t * 2 + 1);
         ++gs;
       }

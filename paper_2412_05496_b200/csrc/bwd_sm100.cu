@@ -777,34 +777,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   block parts the compute warps add), so that exp2(s·c + cterm) = P·scale.
 // Fully masked rows (lse = -inf) and the padding to whole q blocks get cterm = -inf (P = 0).
 template <class ScoreT>
-__global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
-                                      const __nv_bfloat16* __restrict__ dout,
-                                      const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad,
-                                      int D, float scale, ScoreT score, float* __restrict__ cterm,
-                                      float* __restrict__ delta) {
-  const long long row = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) bwd_preprocess_kernel(
+    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+    const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad, int D, float scale, ScoreT score,
+    float* __restrict__ cterm, float* __restrict__ delta, float* __restrict__ dq_acc) {
+  // 8 lanes per row: each lane reads D/8 contiguous bf16 of O and dO with 16-byte loads and
+  // zeroes its D/8 floats of the dQ accumulator (the memset of the fp32 workspace, fused)
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
   if (row >= (long long)BH * Lq_pad) return;
   const int q = (int)(row % Lq_pad);
   const long long bh = row / Lq_pad;
   if (q >= Lq) {
-    if (lane == 0) {
+    if (sub == 0) {
       cterm[row] = -INFINITY;
       delta[row] = 0.f;
     }
     return;
   }
-  const long long src = (bh * Lq + q) * D;
+  const long long src = (bh * Lq + q) * D + sub * (D / 8);
+  const uint4* o4 = reinterpret_cast<const uint4*>(o + src);
+  const uint4* d4 = reinterpret_cast<const uint4*>(dout + src);
+  float4* z4 = reinterpret_cast<float4*>(dq_acc + src);
   float a = 0.f;
-  for (int d = lane * 2; d < D; d += 64) {
-    const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(o + src + d);
-    const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(dout + src + d);
-    a = fmaf(__low2float(x), __low2float(y), a);
-    a = fmaf(__high2float(x), __high2float(y), a);
-  }
+  for (int v = 0; v < D / 64; ++v) {
+    const uint4 x = __ldg(o4 + v), y = __ldg(d4 + v);
+    const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-  if (lane == 0) {
+    for (int e = 0; e < 4; ++e) {
+      a = fmaf(__low2float(xp[e]), __low2float(yp[e]), a);
+      a = fmaf(__high2float(xp[e]), __high2float(yp[e]), a);
+    }
+    z4[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z4[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  a += __shfl_xor_sync(0xffffffffu, a, 4);
+  a += __shfl_xor_sync(0xffffffffu, a, 2);
+  a += __shfl_xor_sync(0xffffffffu, a, 1);
+  if (sub == 0) {
     const float l = lse[bh * Lq + q];
     float ct = l == -INFINITY ? -INFINITY : __log2f(scale) - l * kLog2e;
     if constexpr (ScoreT::kKind == 1)
@@ -814,11 +825,11 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   }
 }
 
-__global__ void dq_convert_kernel(const float4* __restrict__ acc, __nv_bfloat162* __restrict__ dq, long long n4) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    const float4 v = acc[i];
-    dq[2 * i] = __floats2bfloat162_rn(v.x, v.y);
-    dq[2 * i + 1] = __floats2bfloat162_rn(v.z, v.w);
+__global__ void dq_convert_kernel(const float4* __restrict__ acc, uint4* __restrict__ dq, long long n8) {
+  // 8 floats -> 8 bf16 per step: two 16-byte loads, one 16-byte store
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = acc[2 * i], b = acc[2 * i + 1];
+    dq[i] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
   }
 }
 
@@ -834,10 +845,10 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
-  FA_CHECK_CUDA(cudaMemsetAsync(dq_acc, 0, rows * D * 4, st));
-  bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 7) / 8), 256, 0, st>>>(
+  // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
+  bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
-      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta);
+      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
@@ -924,9 +935,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
               cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
               acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, acc[9] / cnt, acc[10] / cnt, acc[11] / cnt);
   }
-  const long long n4 = rows * D / 4;
-  dq_convert_kernel<<<(unsigned)std::min<long long>((n4 + 255) / 256, 148LL * 16), 256, 0, st>>>(
-      reinterpret_cast<const float4*>(dq_acc), static_cast<__nv_bfloat162*>(dq), n4);
+  const long long n8 = rows * D / 8;
+  dq_convert_kernel<<<(unsigned)std::min<long long>((n8 + 255) / 256, 148LL * 16), 256, 0, st>>>(
+      reinterpret_cast<const float4*>(dq_acc), static_cast<uint4*>(dq), n8);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
   return FA_OK;

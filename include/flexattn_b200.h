@@ -69,8 +69,12 @@ enum { FA_F32 = 0, FA_BF16 = 1 };
 /* ---- mask_mod descriptor ----------------------------------------------------
  * A mask is the AND of the primitive terms whose bit is set in `terms`
  * (and_mask, mask_library.cpp:94-98). An empty term set is noop_mask
- * (mask_library.cpp:43-45). Every term sees q + q_offset (offset_mask,
- * mask_library.cpp:106-110).
+ * (mask_library.cpp:43-45). A non-zero `or_terms` adds a second AND-group
+ * evaluated with the same parameters and ORed with the first (or_mask,
+ * mask_library.cpp:100-104). Every term sees q + q_offset (offset_mask,
+ * mask_library.cpp:106-110); with a `remap` table the terms see
+ * (remap[q + q_offset], remap[kv]) (remap_mask, mask_library.cpp:203-215; the
+ * table must be a bijection on [0, remap_len), which the host layers check).
  */
 enum {
   FA_MASK_CAUSAL = 1u << 0,       /* q >= kv                        mask_library.cpp:13-15 */
@@ -78,7 +82,9 @@ enum {
   FA_MASK_DOCUMENT = 1u << 2,     /* ids[q] == ids[kv]              mask_library.cpp:24-34 */
   FA_MASK_PREFIX_LM = 1u << 3,    /* kv < prefix || q >= kv         mask_library.cpp:36-41 */
   FA_MASK_HASH = 1u << 4,         /* test aid hash_mask             tests/test_support.hpp:16-29 */
-  FA_MASK_NEVER = 1u << 5         /* test aid never_mask            tests/test_support.hpp:31-35 */
+  FA_MASK_NEVER = 1u << 5,        /* test aid never_mask            tests/test_support.hpp:31-35 */
+  FA_MASK_NATTEN = 1u << 6        /* 2-D neighbourhood: max(|dr|,|dc|) <= kernel/2 on a
+                                     na_height x na_width canvas      mask_library.cpp:137-149 */
 };
 
 typedef struct fa_mask_desc {
@@ -90,6 +96,12 @@ typedef struct fa_mask_desc {
   uint64_t hash_seed;      /* FA_MASK_HASH */
   const int32_t* doc_ids;  /* FA_MASK_DOCUMENT: device int32[doc_len] */
   int64_t doc_len;
+  uint32_t or_terms;       /* second AND-group, ORed with `terms`; 0 = none (ABI v2) */
+  int32_t na_kernel;       /* FA_MASK_NATTEN: odd, 1 <= kernel <= min(height, width) */
+  int64_t na_height;       /* FA_MASK_NATTEN canvas (tokens = height * width, row-major) */
+  int64_t na_width;
+  const int32_t* remap;    /* optional device int32[remap_len] slot -> token permutation */
+  int64_t remap_len;
 } fa_mask_desc;
 
 /* ---- score_mod descriptor ---------------------------------------------------

@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -130,7 +131,8 @@ inline DeviceTensor4 random_tensor(std::uint64_t seed, i64 b, i64 h, i64 l, i64 
 // ---- modifiers (modifiers.hpp, mask_library.hpp) -------------------------------------------
 struct MaskMod {
   fa_mask_desc d{};
-  std::shared_ptr<void> keep;  // device doc-id table
+  std::shared_ptr<void> keep;        // device doc-id table
+  std::shared_ptr<void> keep_remap;  // device remap table
 };
 struct ScoreMod {
   fa_score_desc d{};
@@ -162,9 +164,90 @@ inline MaskMod and_mask(const MaskMod& a, const MaskMod& b) {
   if (b.d.terms & FA_MASK_PREFIX_LM) m.d.prefix = b.d.prefix;
   if (b.d.terms & FA_MASK_DOCUMENT) { m.d.doc_ids = b.d.doc_ids; m.d.doc_len = b.d.doc_len; m.keep = b.keep; }
   if (b.d.terms & FA_MASK_HASH) { m.d.hash_seed = b.d.hash_seed; m.d.hash_density = b.d.hash_density; }
+  if (b.d.terms & FA_MASK_NATTEN) {
+    m.d.na_height = b.d.na_height; m.d.na_width = b.d.na_width; m.d.na_kernel = b.d.na_kernel;
+  }
   return m;
 }
 inline MaskMod offset_mask(MaskMod m, i64 off) { m.d.q_offset += off; return m; }
+
+// or_mask (mask_library.cpp:100-104) of two single-group masks: the device evaluates
+// (AND of a's terms) OR (AND of b's terms), parameters shared between the groups.
+inline MaskMod or_mask(const MaskMod& a, const MaskMod& b) {
+  if (a.d.or_terms || b.d.or_terms) throw Unsupported("or_mask: operands that are already OR-combinations");
+  if (a.d.remap_len || b.d.remap_len) throw Unsupported("or_mask: remapped operands (apply remap_mask last)");
+  if (a.d.q_offset != b.d.q_offset) throw Unsupported("or_mask: operands with different offsets");
+  if (a.d.terms == 0 || b.d.terms == 0) return noop_mask();  // or with noop is noop
+  MaskMod m = and_mask(a, b);  // merges the parameters of both groups
+  m.d.terms = a.d.terms;
+  m.d.or_terms = b.d.terms;
+  if (b.d.terms & FA_MASK_NATTEN) {
+    m.d.na_height = b.d.na_height; m.d.na_width = b.d.na_width; m.d.na_kernel = b.d.na_kernel;
+  }
+  return m;
+}
+
+// Neighbourhood attention on a canvas_h x canvas_w row-major canvas (mask_library.cpp:121-215).
+struct NAGeometry {
+  i64 canvas_h, canvas_w, kernel;
+  NAGeometry(i64 h, i64 w, i64 k) : canvas_h(h), canvas_w(w), kernel(k) {
+    if (h < 1 || w < 1) throw GeometryMismatch("NAGeometry: canvas dims must be >= 1");
+    if (k < 1 || k % 2 == 0) throw GeometryMismatch("NAGeometry: kernel must be odd and >= 1");
+    if (k > std::min(h, w)) throw GeometryMismatch("NAGeometry: kernel exceeds canvas");
+  }
+  i64 tokens() const { return canvas_h * canvas_w; }
+};
+inline MaskMod na_naive(const NAGeometry& g) {
+  MaskMod m;
+  m.d.terms = FA_MASK_NATTEN;
+  m.d.na_height = g.canvas_h; m.d.na_width = g.canvas_w; m.d.na_kernel = static_cast<int32_t>(g.kernel);
+  return m;
+}
+struct Permutation {
+  std::vector<i64> forward;  // slot -> pixel
+};
+inline Permutation tile_permutation(const NAGeometry& g, i64 tile) {
+  if (tile < 1 || g.canvas_h % tile != 0 || g.canvas_w % tile != 0)
+    throw GeometryMismatch("tile_permutation: tile must divide the canvas");
+  Permutation p;
+  for (i64 tr = 0; tr < g.canvas_h; tr += tile)
+    for (i64 tc = 0; tc < g.canvas_w; tc += tile)
+      for (i64 r = tr; r < tr + tile; ++r)
+        for (i64 c = tc; c < tc + tile; ++c) p.forward.push_back(r * g.canvas_w + c);
+  return p;
+}
+inline Permutation morton_permutation(const NAGeometry& g) {
+  const i64 n = g.canvas_h;
+  if (g.canvas_h != g.canvas_w || (n & (n - 1)) != 0)
+    throw GeometryMismatch("morton_permutation: canvas must be square with power-of-two side");
+  Permutation p;
+  p.forward.assign(static_cast<size_t>(n * n), 0);
+  for (i64 r = 0; r < n; ++r)
+    for (i64 c = 0; c < n; ++c) {
+      i64 slot = 0;
+      for (i64 bit = 0; (i64(1) << bit) < n; ++bit) {
+        slot |= ((c >> bit) & 1) << (2 * bit);
+        slot |= ((r >> bit) & 1) << (2 * bit + 1);
+      }
+      p.forward[static_cast<size_t>(slot)] = r * n + c;
+    }
+  return p;
+}
+// mask(q, kv) = base(fwd[q], fwd[kv]) (mask_library.cpp:203-215)
+inline MaskMod remap_mask(MaskMod base, const Permutation& p) {
+  std::vector<i64> sorted = p.forward;
+  std::sort(sorted.begin(), sorted.end());
+  for (size_t i = 0; i < sorted.size(); ++i)
+    if (sorted[i] != static_cast<i64>(i)) throw GeometryMismatch("Permutation: forward is not a bijection");
+  if (base.d.remap_len) throw Unsupported("remap_mask: base is already remapped");
+  std::vector<int32_t> t32(p.forward.begin(), p.forward.end());
+  DeviceBuffer buf(t32.size() * 4);
+  check_cuda(cudaMemcpy(buf.get(), t32.data(), t32.size() * 4, cudaMemcpyHostToDevice), "remap table");
+  base.d.remap = buf.as<int32_t>();
+  base.d.remap_len = static_cast<i64>(t32.size());
+  base.keep_remap = buf.p;
+  return base;
+}
 
 inline ScoreMod noop_score() { return ScoreMod{}; }
 inline std::vector<double> alibi_slopes(i64 heads) {

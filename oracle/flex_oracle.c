@@ -36,16 +36,19 @@ void fo_random_f32(uint64_t seed, int64_t first, int64_t n, float* out) {
 }
 
 /* ---- mask_mod (mask_library.cpp, tests/test_support.hpp) ----------------- */
-int fo_mask_eval(const fo_mask* m, int64_t b, int64_t h, int64_t q, int64_t kv, int* out) {
-  /* bound_mask (block_mask.cpp:14-19) is applied on the UNshifted q, then the
-   * user mask sees q + offset (decode runtime mask, engine.cpp:421-424). */
-  if (m->bound_q > 0 && !(q < m->bound_q)) { *out = 0; return OK; }
-  if (m->bound_kv > 0 && !(kv < m->bound_kv)) { *out = 0; return OK; }
-  const int64_t qq = q + m->q_offset; /* offset_mask (mask_library.cpp:106-110) */
-  const uint32_t t = m->terms;
+/* AND of the primitive terms in t at positions (q, kv) (and_mask, mask_library.cpp:94-98) */
+static int mask_group(const fo_mask* m, uint32_t t, int64_t b, int64_t h, int64_t qq, int64_t kv,
+                      int* out) {
   if (t & (1u << 5)) { *out = 0; return OK; } /* never_mask, test_support.hpp:31-35 */
   if ((t & 1u) && !(qq >= kv)) { *out = 0; return OK; }                       /* causal :13-15 */
   if ((t & 2u) && !(qq >= kv && qq - kv <= m->window)) { *out = 0; return OK; } /* sliding :17-22 */
+  if (t & 64u) {                                                              /* na_naive :137-149 */
+    const int64_t w = m->na_width, n = m->na_height * m->na_width, rad = m->na_kernel / 2;
+    if (qq < 0 || qq >= n || kv < 0 || kv >= n) return E_INDEX;
+    const int64_t dr = qq / w - kv / w, dc = qq % w - kv % w;
+    const int64_t adr = dr < 0 ? -dr : dr, adc = dc < 0 ? -dc : dc;
+    if (!((adr > adc ? adr : adc) <= rad)) { *out = 0; return OK; }
+  }
   if (t & 4u) {                                                                 /* document :24-34 */
     const int64_t n = m->doc_len;
     if (qq < 0 || qq >= n || kv < 0 || kv >= n) return E_INDEX;
@@ -65,6 +68,23 @@ int fo_mask_eval(const fo_mask* m, int64_t b, int64_t h, int64_t q, int64_t kv, 
   }
   *out = 1;
   return OK;
+}
+
+int fo_mask_eval(const fo_mask* m, int64_t b, int64_t h, int64_t q, int64_t kv, int* out) {
+  /* bound_mask (block_mask.cpp:14-19) is applied on the UNshifted q, then the
+   * user mask sees q + offset (decode runtime mask, engine.cpp:421-424). */
+  if (m->bound_q > 0 && !(q < m->bound_q)) { *out = 0; return OK; }
+  if (m->bound_kv > 0 && !(kv < m->bound_kv)) { *out = 0; return OK; }
+  int64_t qq = q + m->q_offset; /* offset_mask (mask_library.cpp:106-110) */
+  if (m->remap_len > 0) {      /* remap_mask (mask_library.cpp:203-215) */
+    if (qq < 0 || qq >= m->remap_len || kv < 0 || kv >= m->remap_len) return E_INDEX;
+    qq = m->remap[qq];
+    kv = m->remap[kv];
+  }
+  int st = mask_group(m, m->terms, b, h, qq, kv, out);
+  if (st != OK) return st;
+  if (!*out && m->or_terms != 0) st = mask_group(m, m->or_terms, b, h, qq, kv, out); /* or_mask :100-104 */
+  return st;
 }
 
 /* ---- score_mod (mask_library.cpp:47-92, modifiers.hpp:57-66) ------------ */

@@ -31,6 +31,12 @@ typedef struct fo_mask {
   int64_t doc_len;
   int64_t bound_q;          /* > 0: runtime mask adds q < bound_q (bound_mask, block_mask.cpp:14-19) */
   int64_t bound_kv;         /* > 0: ... && kv < bound_kv */
+  uint32_t or_terms;        /* second AND-group, ORed (or_mask) */
+  int32_t na_kernel;        /* term 64: na_naive on a na_height x na_width canvas */
+  int64_t na_height;
+  int64_t na_width;
+  const int64_t* remap;     /* host; remap_mask slot -> token, or NULL */
+  int64_t remap_len;
 } fo_mask;
 
 typedef struct fo_score {

@@ -27,6 +27,7 @@ PORT_PATH = os.path.join(HERE, "libflex_oracle.so")
 REF_PATH = os.path.join(HERE, "_ref", "libblockattn_ref.so")
 
 MASK_CAUSAL, MASK_SLIDING, MASK_DOCUMENT, MASK_PREFIX, MASK_HASH, MASK_NEVER = 1, 2, 4, 8, 16, 32
+MASK_NATTEN = 64
 SCORE_ALIBI, SCORE_SOFTCAP = 1, 2
 
 
@@ -34,7 +35,9 @@ class _FoMask(C.Structure):
     _fields_ = [("terms", C.c_uint32), ("hash_density", C.c_int32), ("window", C.c_int64),
                 ("prefix", C.c_int64), ("q_offset", C.c_int64), ("hash_seed", C.c_uint64),
                 ("doc_ids", C.POINTER(C.c_int64)), ("doc_len", C.c_int64),
-                ("bound_q", C.c_int64), ("bound_kv", C.c_int64)]
+                ("bound_q", C.c_int64), ("bound_kv", C.c_int64),
+                ("or_terms", C.c_uint32), ("na_kernel", C.c_int32), ("na_height", C.c_int64),
+                ("na_width", C.c_int64), ("remap", C.POINTER(C.c_int64)), ("remap_len", C.c_int64)]
 
 
 class _FoScore(C.Structure):
@@ -51,7 +54,8 @@ class _FoBm(C.Structure):
 
 @dataclass
 class Mask:
-    """AND of primitive mask terms (same bits as fa_mask_desc)."""
+    """AND of primitive mask terms, optionally ORed with a second group and remapped
+    (same bits and meaning as fa_mask_desc)."""
     terms: int = 0
     window: int = 0
     prefix: int = 0
@@ -59,6 +63,11 @@ class Mask:
     hash_seed: int = 0
     hash_density: int = 128
     doc_ids: Optional[np.ndarray] = None
+    or_terms: int = 0
+    na_height: int = 0
+    na_width: int = 0
+    na_kernel: int = 0
+    remap: Optional[np.ndarray] = None
 
     def c(self, bound_q: int = 0, bound_kv: int = 0) -> _FoMask:
         m = _FoMask()
@@ -74,6 +83,12 @@ class Mask:
             m.doc_len = len(self._ids)
         m.bound_q = bound_q
         m.bound_kv = bound_kv
+        m.or_terms = self.or_terms
+        m.na_height, m.na_width, m.na_kernel = self.na_height, self.na_width, self.na_kernel
+        if self.remap is not None:
+            self._remap = np.ascontiguousarray(self.remap, dtype=np.int64)
+            m.remap = self._remap.ctypes.data_as(C.POINTER(C.c_int64))
+            m.remap_len = len(self._remap)
         return m
 
 
@@ -107,6 +122,55 @@ def sliding_window(w: int) -> Mask:
 def document(ids, and_causal: bool = False) -> Mask:
     return Mask(terms=MASK_DOCUMENT | (MASK_CAUSAL if and_causal else 0),
                 doc_ids=np.asarray(ids, dtype=np.int64))
+
+
+def na_naive(h: int, w: int, kernel: int) -> Mask:
+    """na_naive(NAGeometry(h, w, kernel)) (mask_library.cpp:137-149)."""
+    return Mask(terms=MASK_NATTEN, na_height=h, na_width=w, na_kernel=kernel)
+
+
+def tile_permutation_np(h: int, w: int, tile: int) -> np.ndarray:
+    """Restatement of tile_permutation (mask_library.cpp:164-181): tiles in row-major order,
+    pixels row-major within a tile."""
+    out = []
+    for tr in range(0, h, tile):
+        for tc in range(0, w, tile):
+            for r in range(tr, tr + tile):
+                for c in range(tc, tc + tile):
+                    out.append(r * w + c)
+    return np.asarray(out, dtype=np.int64)
+
+
+def morton_permutation_np(n_side: int) -> np.ndarray:
+    """Restatement of morton_permutation (mask_library.cpp:183-201): slot = bit interleave
+    of (row, col), col bits in the even positions."""
+    out = np.zeros(n_side * n_side, dtype=np.int64)
+    bits = max(1, (n_side - 1).bit_length())
+    for r in range(n_side):
+        for c in range(n_side):
+            slot = 0
+            for b in range(bits):
+                if (1 << b) >= n_side:
+                    break
+                slot |= ((c >> b) & 1) << (2 * b)
+                slot |= ((r >> b) & 1) << (2 * b + 1)
+            out[slot] = r * n_side + c
+    return out
+
+
+def ref_tile_permutation(h: int, w: int, kernel: int, tile: int) -> np.ndarray:
+    lib = ref()
+    out = np.zeros(h * w, dtype=np.int64)
+    _check(lib.ref_tile_permutation(C.c_int64(h), C.c_int64(w), C.c_int64(kernel), C.c_int64(tile),
+                                    _p(out, C.c_int64)), lib)
+    return out
+
+
+def ref_morton_permutation(h: int, w: int, kernel: int) -> np.ndarray:
+    lib = ref()
+    out = np.zeros(h * w, dtype=np.int64)
+    _check(lib.ref_morton_permutation(C.c_int64(h), C.c_int64(w), C.c_int64(kernel), _p(out, C.c_int64)), lib)
+    return out
 
 
 def alibi_slopes(heads: int) -> np.ndarray:

@@ -41,6 +41,12 @@ struct RefMask {  // same field order as fo_mask (oracle/flex_oracle.h)
   int64_t doc_len;
   int64_t bound_q;
   int64_t bound_kv;
+  uint32_t or_terms;
+  int32_t na_kernel;
+  int64_t na_height;
+  int64_t na_width;
+  const int64_t* remap;
+  int64_t remap_len;
 };
 
 struct RefScore {  // same field order as fo_score
@@ -51,20 +57,33 @@ struct RefScore {  // same field order as fo_score
   int64_t q_offset;
 };
 
-// Build the user mask as the reference library would (and_mask of terms).
-MaskMod make_mask(const RefMask& d, bool with_offset = true) {
+// Build the user mask as the reference library would: and_mask of the terms, or_mask with the
+// second term group, remap_mask around both, offset_mask outermost.
+MaskMod make_group(const RefMask& d, uint32_t terms) {
   MaskMod m = noop_mask();
   bool have = false;
   auto add = [&](MaskMod t) {
     m = have ? and_mask(m, t) : t;
     have = true;
   };
-  if (d.terms & 32u) add(testsupport::never_mask());
-  if (d.terms & 1u) add(causal());
-  if (d.terms & 2u) add(sliding_window(d.window));
-  if (d.terms & 4u) add(document_mask(std::vector<i64>(d.doc_ids, d.doc_ids + d.doc_len)));
-  if (d.terms & 8u) add(prefix_lm(d.prefix));
-  if (d.terms & 16u) add(testsupport::hash_mask(d.hash_seed, d.hash_density));
+  if (terms & 32u) add(testsupport::never_mask());
+  if (terms & 1u) add(causal());
+  if (terms & 2u) add(sliding_window(d.window));
+  if (terms & 64u) add(na_naive(NAGeometry(d.na_height, d.na_width, d.na_kernel)));
+  if (terms & 4u) add(document_mask(std::vector<i64>(d.doc_ids, d.doc_ids + d.doc_len)));
+  if (terms & 8u) add(prefix_lm(d.prefix));
+  if (terms & 16u) add(testsupport::hash_mask(d.hash_seed, d.hash_density));
+  return m;
+}
+
+MaskMod make_mask(const RefMask& d, bool with_offset = true) {
+  MaskMod m = make_group(d, d.terms);
+  if (d.or_terms != 0) m = or_mask(m, make_group(d, d.or_terms));
+  if (d.remap_len > 0) {
+    Permutation p;
+    p.forward.assign(d.remap, d.remap + d.remap_len);
+    m = remap_mask(m, p);
+  }
   if (with_offset && d.q_offset != 0) m = offset_mask(m, d.q_offset);
   return m;
 }
@@ -170,6 +189,26 @@ int do_backward(const Real* q, const Real* k, const Real* v, const Real* dout, i
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// tile_permutation / morton_permutation (mask_library.cpp:164-201): forward table into out[h*w]
+int ref_tile_permutation(int64_t h, int64_t w, int64_t k, int64_t tile, int64_t* out) {
+  try {
+    const auto p = tile_permutation(NAGeometry(h, w, k), tile);
+    std::copy(p.forward.begin(), p.forward.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+int ref_morton_permutation(int64_t h, int64_t w, int64_t k, int64_t* out) {
+  try {
+    const auto p = morton_permutation(NAGeometry(h, w, k));
+    std::copy(p.forward.begin(), p.forward.end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
 int ref_worker_count() { return worker_count(); }
 
 // create_block_mask (+ transpose) with all seven arrays (block_mask.hpp:109-115).

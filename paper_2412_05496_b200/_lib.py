@@ -19,7 +19,9 @@ FA_F32, FA_BF16 = 0, 1
 class MaskDesc(C.Structure):
     _fields_ = [("terms", C.c_uint32), ("hash_density", C.c_int32), ("window", C.c_int64),
                 ("prefix", C.c_int64), ("q_offset", C.c_int64), ("hash_seed", C.c_uint64),
-                ("doc_ids", C.c_void_p), ("doc_len", C.c_int64)]
+                ("doc_ids", C.c_void_p), ("doc_len", C.c_int64),
+                ("or_terms", C.c_uint32), ("na_kernel", C.c_int32), ("na_height", C.c_int64),
+                ("na_width", C.c_int64), ("remap", C.c_void_p), ("remap_len", C.c_int64)]
 
 
 class ScoreDesc(C.Structure):

@@ -68,12 +68,14 @@ def _stream() -> int:
 
 # ---------------------------------------------------------------- modifiers (mask_library.hpp)
 MASK_CAUSAL, MASK_SLIDING, MASK_DOCUMENT, MASK_PREFIX, MASK_HASH, MASK_NEVER = 1, 2, 4, 8, 16, 32
+MASK_NATTEN = 64
 SCORE_ALIBI, SCORE_SOFT_CAP = 1, 2
 
 
 @dataclass(frozen=True)
 class MaskMod:
-    """A mask_mod: AND of primitive terms (and_mask) with an optional q offset."""
+    """A mask_mod: AND of primitive terms (and_mask), optionally ORed with a second term group
+    (or_mask) and evaluated on permuted positions (remap_mask), with an optional q offset."""
     terms: int = 0
     window: int = 0
     prefix: int = 0
@@ -81,15 +83,26 @@ class MaskMod:
     hash_seed: int = 0
     hash_density: int = 128
     doc_ids: Optional[torch.Tensor] = field(default=None, compare=False)
+    or_terms: int = 0
+    na_height: int = 0
+    na_width: int = 0
+    na_kernel: int = 0
+    remap: Optional[torch.Tensor] = field(default=None, compare=False)
 
     def desc(self, device) -> MaskDesc:
         d = MaskDesc()
         d.terms, d.window, d.prefix, d.q_offset = self.terms, self.window, self.prefix, self.q_offset
         d.hash_seed, d.hash_density = self.hash_seed, self.hash_density
+        d.or_terms = self.or_terms
+        d.na_height, d.na_width, d.na_kernel = self.na_height, self.na_width, self.na_kernel
         if self.doc_ids is not None:
             ids = _device_cache(self, "doc_ids", self.doc_ids, torch.int32, device)
             d.doc_ids = ids.data_ptr()
             d.doc_len = ids.numel()
+        if self.remap is not None:
+            rm = _device_cache(self, "remap", self.remap, torch.int32, device)
+            d.remap = rm.data_ptr()
+            d.remap_len = rm.numel()
         return d
 
 
@@ -168,19 +181,110 @@ def never_mask() -> MaskMod:
     return MaskMod(terms=MASK_NEVER)
 
 
-def and_mask(a: MaskMod, b: MaskMod) -> MaskMod:
-    """and_mask (mask_library.cpp:94-98) for masks expressible as one term set."""
+def _merge_params(a: MaskMod, b: MaskMod, what: str) -> dict:
     if a.q_offset != b.q_offset:
-        raise Unsupported("and_mask: operands with different offsets")
+        raise Unsupported(f"{what}: operands with different offsets")
+    if a.remap is not None or b.remap is not None:
+        raise Unsupported(f"{what}: remapped operands (apply remap_mask last)")
     for attr in ("window", "prefix", "hash_seed"):
         if getattr(a, attr) and getattr(b, attr) and getattr(a, attr) != getattr(b, attr):
-            raise Unsupported(f"and_mask: conflicting {attr}")
+            raise Unsupported(f"{what}: conflicting {attr}")
+    if (a.terms | a.or_terms) & MASK_NATTEN and (b.terms | b.or_terms) & MASK_NATTEN and \
+            (a.na_height, a.na_width, a.na_kernel) != (b.na_height, b.na_width, b.na_kernel):
+        raise Unsupported(f"{what}: two different neighbourhood geometries")
     if a.doc_ids is not None and b.doc_ids is not None:
-        raise Unsupported("and_mask: two document masks")
-    hd = a.hash_density if a.terms & MASK_HASH else b.hash_density
-    return MaskMod(terms=a.terms | b.terms, window=a.window or b.window, prefix=a.prefix or b.prefix,
-                   q_offset=a.q_offset, hash_seed=a.hash_seed or b.hash_seed, hash_density=hd,
-                   doc_ids=a.doc_ids if a.doc_ids is not None else b.doc_ids)
+        raise Unsupported(f"{what}: two document masks")
+    na = a if (a.terms | a.or_terms) & MASK_NATTEN else b
+    hd = a.hash_density if (a.terms | a.or_terms) & MASK_HASH else b.hash_density
+    return dict(window=a.window or b.window, prefix=a.prefix or b.prefix, q_offset=a.q_offset,
+                hash_seed=a.hash_seed or b.hash_seed, hash_density=hd,
+                doc_ids=a.doc_ids if a.doc_ids is not None else b.doc_ids,
+                na_height=na.na_height, na_width=na.na_width, na_kernel=na.na_kernel)
+
+
+def or_mask(a: MaskMod, b: MaskMod) -> MaskMod:
+    """or_mask (mask_library.cpp:100-104) of two single-group masks: the device evaluates
+    (AND of a's terms) OR (AND of b's terms) with shared parameters."""
+    if a.or_terms or b.or_terms:
+        raise Unsupported("or_mask: operands that are already OR-combinations")
+    kw = _merge_params(a, b, "or_mask")
+    if a.terms == 0 or b.terms == 0:  # or with noop_mask is noop_mask
+        return MaskMod(**kw)
+    return MaskMod(terms=a.terms, or_terms=b.terms, **kw)
+
+
+@dataclass(frozen=True)
+class NAGeometry:
+    """Neighbourhood-attention canvas (mask_library.hpp NAGeometry, mask_library.cpp:121-135):
+    tokens are the pixels of a height x width canvas in row-major order."""
+    canvas_h: int
+    canvas_w: int
+    kernel: int
+
+    def __post_init__(self):
+        if self.canvas_h < 1 or self.canvas_w < 1:
+            raise GeometryMismatch(f"NAGeometry: canvas dims must be >= 1, got {self.canvas_h}x{self.canvas_w}")
+        if self.kernel < 1 or self.kernel % 2 == 0:
+            raise GeometryMismatch(f"NAGeometry: kernel must be odd and >= 1, got {self.kernel}")
+        if self.kernel > min(self.canvas_h, self.canvas_w):
+            raise GeometryMismatch(f"NAGeometry: kernel {self.kernel} exceeds canvas "
+                                   f"{self.canvas_h}x{self.canvas_w}")
+
+    def tokens(self) -> int:
+        return self.canvas_h * self.canvas_w
+
+
+def na_naive(g: NAGeometry) -> MaskMod:
+    """2-D neighbourhood attention: max(|dr|, |dc|) <= kernel // 2 (mask_library.cpp:137-149)."""
+    return MaskMod(terms=MASK_NATTEN, na_height=g.canvas_h, na_width=g.canvas_w, na_kernel=g.kernel)
+
+
+def tile_permutation(g: NAGeometry, tile: int) -> list:
+    """Slot -> pixel table visiting tile x tile squares in row-major order, pixels row-major
+    inside a tile (mask_library.cpp:164-181)."""
+    if tile < 1 or g.canvas_h % tile or g.canvas_w % tile:
+        raise GeometryMismatch(f"tile_permutation: tile {tile} must divide canvas {g.canvas_h}x{g.canvas_w}")
+    return [r * g.canvas_w + c
+            for tr in range(0, g.canvas_h, tile) for tc in range(0, g.canvas_w, tile)
+            for r in range(tr, tr + tile) for c in range(tc, tc + tile)]
+
+
+def morton_permutation(g: NAGeometry) -> list:
+    """Slot -> pixel table in Z (Morton) order, column bits in the even positions
+    (mask_library.cpp:183-201); square power-of-two canvases only."""
+    n = g.canvas_h
+    if g.canvas_h != g.canvas_w or n & (n - 1):
+        raise GeometryMismatch(f"morton_permutation: canvas must be square with power-of-two side, "
+                               f"got {g.canvas_h}x{g.canvas_w}")
+    out = [0] * (n * n)
+    for r in range(n):
+        for c in range(n):
+            slot, bit = 0, 0
+            while (1 << bit) < n:
+                slot |= ((c >> bit) & 1) << (2 * bit)
+                slot |= ((r >> bit) & 1) << (2 * bit + 1)
+                bit += 1
+            out[slot] = r * n + c
+    return out
+
+
+def remap_mask(base: MaskMod, forward_table) -> MaskMod:
+    """mask(q, kv) = base(fwd[q], fwd[kv]) (mask_library.cpp:203-215); the table must be a
+    bijection on [0, len) (GeometryMismatch otherwise)."""
+    fwd = [int(x) for x in forward_table]
+    if sorted(fwd) != list(range(len(fwd))):
+        raise GeometryMismatch(f"Permutation: forward is not a bijection on [0, {len(fwd)})")
+    if base.remap is not None:
+        raise Unsupported("remap_mask: base is already remapped")
+    return replace(base, remap=torch.tensor(fwd, dtype=torch.int32))
+
+
+def and_mask(a: MaskMod, b: MaskMod) -> MaskMod:
+    """and_mask (mask_library.cpp:94-98) for masks expressible as one term set."""
+    if a.or_terms or b.or_terms:
+        raise Unsupported("and_mask: OR-combined operands")
+    kw = _merge_params(a, b, "and_mask")
+    return MaskMod(terms=a.terms | b.terms, **kw)
 
 
 def offset_mask(m: MaskMod, offset: int) -> MaskMod:

@@ -152,19 +152,7 @@ int grid_for(long long warps_needed) {
 }
 
 fa_status validate_mask_desc(const fa_mask_desc& m, int64_t q_len, int64_t kv_len) {
-  FA_REQUIRE(!(m.terms & ~0x3Fu), FA_SHAPE_MISMATCH, "mask: unknown term bits");
-  if (m.terms & kMaskSliding)
-    FA_REQUIRE(m.window >= 0, FA_INDEX_OUT_OF_RANGE, "sliding_window: window must be >= 0");
-  if (m.terms & kMaskPrefix)
-    FA_REQUIRE(m.prefix >= 0, FA_INDEX_OUT_OF_RANGE, "prefix_lm: prefix_len must be >= 0");
-  if (m.terms & kMaskDocument) {
-    FA_REQUIRE(m.doc_ids != nullptr, FA_SHAPE_MISMATCH, "document_mask: doc_ids is NULL");
-    // the reference throws IndexOutOfRange on the first out-of-table index (mask_library.cpp:27-31)
-    FA_REQUIRE(m.doc_len >= q_len + m.q_offset && m.doc_len >= kv_len && q_len + m.q_offset > 0,
-               FA_INDEX_OUT_OF_RANGE,
-               "document_mask: token index outside id table of size " + std::to_string(m.doc_len));
-  }
-  return FA_OK;
+  return check_mask_desc(m, q_len, kv_len);
 }
 
 }  // namespace
@@ -244,7 +232,7 @@ extern "C" fa_status fa_create_block_mask(const fa_mask_desc* mask, int64_t b_di
   uint8_t* grid = static_cast<uint8_t*>(workspace);
   const MaskParams mp = to_mask_params(*mask);
   const int bd = (int)b_dims, hd = (int)h_dims, R = (int)rows, Cc = (int)cols;
-  switch (mask_kind_of(mask->terms)) {
+  switch (mask_kind_of(*mask)) {
     case kMaskNoop: launch_classify(MaskFn<kMaskNoop>{mp}, bd, hd, R, Cc, (int)q_len, (int)kv_len, (int)bs_q, (int)bs_kv, grid, st); break;
     case kMaskCausalOnly: launch_classify(MaskFn<kMaskCausalOnly>{mp}, bd, hd, R, Cc, (int)q_len, (int)kv_len, (int)bs_q, (int)bs_kv, grid, st); break;
     case kMaskSlidingOnly: launch_classify(MaskFn<kMaskSlidingOnly>{mp}, bd, hd, R, Cc, (int)q_len, (int)kv_len, (int)bs_q, (int)bs_kv, grid, st); break;

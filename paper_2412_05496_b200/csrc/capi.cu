@@ -42,6 +42,11 @@ MaskParams to_mask_params(const fa_mask_desc& d) {
   m.doc_len = static_cast<int32_t>(d.doc_len);
   m.hash_seed = d.hash_seed;
   m.doc_ids = d.doc_ids;
+  m.or_terms = d.or_terms;
+  m.na_w = static_cast<int32_t>(d.na_width);
+  m.na_n = static_cast<int32_t>(d.na_height * d.na_width);
+  m.na_radius = d.na_kernel / 2;
+  m.remap = d.remap_len > 0 ? d.remap : nullptr;
   return m;
 }
 
@@ -55,12 +60,53 @@ ScoreParams to_score_params(const fa_score_desc& d) {
   return s;
 }
 
-int mask_kind_of(uint32_t terms) {
+int mask_kind_of(const fa_mask_desc& d) {
+  if (d.or_terms != 0 || d.remap_len > 0) return kMaskDynamic;
+  const uint32_t terms = d.terms;
   if (terms == 0) return kMaskNoop;
   if (terms == kMaskCausal) return kMaskCausalOnly;
   if (terms == kMaskSliding || terms == (kMaskSliding | kMaskCausal)) return kMaskSlidingOnly;
   if (terms == (kMaskDocument | kMaskCausal)) return kMaskDocCausal;
   return kMaskDynamic;
+}
+
+// Checks of the mask terms that the reference performs when it builds or evaluates the
+// mask (GeometryMismatch / IndexOutOfRange): positions q in [q_offset, q_len + q_offset),
+// kv in [0, kv_len) must be inside every table the terms index.
+fa_status check_mask_desc(const fa_mask_desc& m, int64_t q_len, int64_t kv_len) {
+  FA_REQUIRE(!(m.terms & ~0x7Fu) && !(m.or_terms & ~0x7Fu), FA_SHAPE_MISMATCH, "mask: unknown term bits");
+  const uint32_t all = m.terms | m.or_terms;
+  if (all & kMaskSliding)
+    FA_REQUIRE(m.window >= 0, FA_INDEX_OUT_OF_RANGE, "sliding_window: window must be >= 0");
+  if (all & kMaskPrefix)
+    FA_REQUIRE(m.prefix >= 0, FA_INDEX_OUT_OF_RANGE, "prefix_lm: prefix_len must be >= 0");
+  const int64_t q_end = q_len + m.q_offset;
+  if (m.remap_len > 0) {  // remap_mask range check, mask_library.cpp:208-211
+    FA_REQUIRE(m.remap != nullptr, FA_SHAPE_MISMATCH, "remap_mask: table is NULL");
+    FA_REQUIRE(m.q_offset >= 0 && q_end <= m.remap_len && kv_len <= m.remap_len, FA_INDEX_OUT_OF_RANGE,
+               "remap_mask: slot index outside permutation of size " + std::to_string(m.remap_len));
+  }
+  // with a remap the terms see permuted tokens in [0, remap_len)
+  const int64_t q_hi = m.remap_len > 0 ? m.remap_len : q_end;
+  const int64_t kv_hi = m.remap_len > 0 ? m.remap_len : kv_len;
+  if (all & kMaskDocument) {
+    FA_REQUIRE(m.doc_ids != nullptr, FA_SHAPE_MISMATCH, "document_mask: doc_ids is NULL");
+    // the reference throws IndexOutOfRange on the first out-of-table index (mask_library.cpp:27-31)
+    FA_REQUIRE(m.doc_len >= q_hi && m.doc_len >= kv_hi && q_end > 0, FA_INDEX_OUT_OF_RANGE,
+               "document_mask: token index outside id table of size " + std::to_string(m.doc_len));
+  }
+  if (all & kMaskNatten) {  // NAGeometry, mask_library.cpp:121-135; na_naive range :141-144
+    FA_REQUIRE(m.na_height >= 1 && m.na_width >= 1, FA_GEOMETRY_MISMATCH,
+               "NAGeometry: canvas dims must be >= 1");
+    FA_REQUIRE(m.na_kernel >= 1 && m.na_kernel % 2 == 1, FA_GEOMETRY_MISMATCH,
+               "NAGeometry: kernel must be odd and >= 1");
+    FA_REQUIRE(m.na_kernel <= std::min(m.na_height, m.na_width), FA_GEOMETRY_MISMATCH,
+               "NAGeometry: kernel exceeds canvas");
+    const int64_t n = m.na_height * m.na_width;
+    FA_REQUIRE(q_hi <= n && kv_hi <= n && m.q_offset >= 0, FA_INDEX_OUT_OF_RANGE,
+               "na_naive: token index outside canvas of " + std::to_string(n) + " pixels");
+  }
+  return FA_OK;
 }
 
 }  // namespace fa
@@ -120,17 +166,9 @@ fa_status check_bm(const fa_block_mask* bm, int64_t batch, int64_t heads, int64_
 
 fa_status check_mods(const fa_mask_desc& m, const fa_score_desc& s, int64_t heads, int64_t q_len,
                      int64_t kv_len) {
-  FA_REQUIRE(!(m.terms & ~0x3Fu), FA_SHAPE_MISMATCH, "mask: unknown term bits");
   FA_REQUIRE(!(s.terms & ~0x3u), FA_SHAPE_MISMATCH, "score: unknown term bits");
-  if (m.terms & kMaskSliding)
-    FA_REQUIRE(m.window >= 0, FA_INDEX_OUT_OF_RANGE, "sliding_window: window must be >= 0");
-  if (m.terms & kMaskPrefix)
-    FA_REQUIRE(m.prefix >= 0, FA_INDEX_OUT_OF_RANGE, "prefix_lm: prefix_len must be >= 0");
-  if (m.terms & kMaskDocument) {
-    FA_REQUIRE(m.doc_ids != nullptr, FA_SHAPE_MISMATCH, "document_mask: doc_ids is NULL");
-    FA_REQUIRE(m.doc_len >= q_len + m.q_offset && m.doc_len >= kv_len, FA_INDEX_OUT_OF_RANGE,
-               "document_mask: token index outside id table of size " + std::to_string(m.doc_len));
-  }
+  fa_status st;
+  if ((st = check_mask_desc(m, q_len, kv_len)) != FA_OK) return st;
   if (s.terms & kScoreAlibi) {
     FA_REQUIRE(s.slopes != nullptr, FA_SHAPE_MISMATCH, "alibi: slopes is NULL");
     FA_REQUIRE(s.num_slopes >= heads, FA_INDEX_OUT_OF_RANGE,
@@ -163,7 +201,7 @@ BmView kv_view(const fa_block_mask* bm) {
 extern "C" {
 
 const char* fa_last_error(void) { return g_last_error.c_str(); }
-int32_t fa_abi_version(void) { return 1; }
+int32_t fa_abi_version(void) { return 2; }  // v2: fa_mask_desc or_terms / natten / remap
 uint64_t fa_launch_count(void) { return g_launches.load(); }
 
 const char* fa_status_name(fa_status s) {
@@ -201,7 +239,7 @@ fa_status fa_flex_fwd(const fa_fwd_args* a, void* stream) {
   const AttnGeom g = geom_of(a->q, a->k, a->bm, a->scale, a->gqa_group);
   const MaskParams mp = to_mask_params(a->mask);
   const ScoreParams sp = to_score_params(a->score);
-  const int mk = mask_kind_of(a->mask.terms);
+  const int mk = mask_kind_of(a->mask);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (a->q.dtype == FA_BF16 && fwd_sm100_supported(g))
     return launch_fwd_sm100(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, kv_view(a->bm),
@@ -246,7 +284,7 @@ fa_status fa_flex_bwd(const fa_bwd_args* a, void* stream) {
                    a->bm->full_q_indices};
   return launch_bwd(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->d_out.data,
                     a->dq.data, a->dk.data, a->dv.data, a->q.dtype, kv_view(a->bm), bmt,
-                    to_mask_params(a->mask), mask_kind_of(a->mask.terms),
+                    to_mask_params(a->mask), mask_kind_of(a->mask),
                     to_score_params(a->score), (int)a->score.terms, a->workspace,
                     static_cast<cudaStream_t>(stream));
 }
@@ -320,7 +358,7 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
     pv.enabled = 1;
   }
   return launch_decode(g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse,
-                       kv_view(a->bm), pv, to_mask_params(m), mask_kind_of(m.terms),
+                       kv_view(a->bm), pv, to_mask_params(m), mask_kind_of(m),
                        to_score_params(sc), (int)sc.terms, a->workspace,
                        static_cast<cudaStream_t>(stream));
 }

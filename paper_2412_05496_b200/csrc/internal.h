@@ -34,8 +34,10 @@ int num_sms();
 // Host mirror of the descriptors (validated, device pointers).
 MaskParams to_mask_params(const fa_mask_desc& d);
 ScoreParams to_score_params(const fa_score_desc& d);
-// Pick the specialised kernel kind for a term set (kMaskDynamic if none matches).
-int mask_kind_of(uint32_t terms);
+// Pick the specialised kernel kind for a mask (kMaskDynamic if none matches).
+int mask_kind_of(const fa_mask_desc& d);
+// Reference-equivalent checks of a mask descriptor for q in [0, q_len), kv in [0, kv_len).
+fa_status check_mask_desc(const fa_mask_desc& m, int64_t q_len, int64_t kv_len);
 
 // Geometry of the forward problem, shared by the launchers.
 struct AttnGeom {

@@ -28,6 +28,9 @@ struct MaskParams {
   int32_t doc_len;
   uint64_t hash_seed;
   const int32_t* doc_ids;
+  uint32_t or_terms;       // second AND-group (or_mask)
+  int32_t na_w, na_n, na_radius;  // neighbourhood attention canvas (width, tokens, kernel / 2)
+  const int32_t* remap;    // slot -> token (remap_mask), or null
 };
 
 struct ScoreParams {
@@ -45,6 +48,7 @@ enum : uint32_t {
   kMaskPrefix = 1u << 3,
   kMaskHash = 1u << 4,
   kMaskNever = 1u << 5,
+  kMaskNatten = 1u << 6,
 };
 
 // Specialised mask kinds the kernels are instantiated for; kMaskDynamic
@@ -162,16 +166,30 @@ struct MaskFn {
       // validated on the host before launch (the reference throws IndexOutOfRange).
       return qq >= kv && __ldg(p.doc_ids + qq) == __ldg(p.doc_ids + kv);
     } else {
-      const uint32_t t = p.terms;
-      bool ok = true;
-      if (t & kMaskNever) ok = false;
-      if (t & kMaskCausal) ok = ok && (qq >= kv);
-      if (t & kMaskSliding) ok = ok && (qq >= kv && qq - kv <= p.window);
-      if (t & kMaskPrefix) ok = ok && (kv < p.prefix || qq >= kv);  // prefix_lm :36-41
-      if ((t & kMaskDocument) && ok) ok = __ldg(p.doc_ids + qq) == __ldg(p.doc_ids + kv);
-      if ((t & kMaskHash) && ok) ok = hash_mask_eval(p.hash_seed, p.hash_density, b, h, qq, kv);
+      int qs = qq, ks = kv;
+      if (p.remap != nullptr) {  // remap_mask, mask_library.cpp:203-215
+        qs = __ldg(p.remap + qq);
+        ks = __ldg(p.remap + kv);
+      }
+      bool ok = group(p.terms, b, h, qs, ks);
+      if (p.or_terms != 0u && !ok) ok = group(p.or_terms, b, h, qs, ks);  // or_mask :100-104
       return ok;
     }
+  }
+  // AND of the primitive terms in t at (already offset / remapped) positions q, kv
+  __device__ __forceinline__ bool group(uint32_t t, int b, int h, int q, int kv) const {
+    bool ok = true;
+    if (t & kMaskNever) ok = false;
+    if (t & kMaskCausal) ok = ok && (q >= kv);
+    if (t & kMaskSliding) ok = ok && (q >= kv && q - kv <= p.window);
+    if (t & kMaskPrefix) ok = ok && (kv < p.prefix || q >= kv);  // prefix_lm :36-41
+    if ((t & kMaskNatten) && ok) {  // na_naive, mask_library.cpp:137-149
+      const int dr = q / p.na_w - kv / p.na_w, dc = q % p.na_w - kv % p.na_w;
+      ok = max(abs(dr), abs(dc)) <= p.na_radius;
+    }
+    if ((t & kMaskDocument) && ok) ok = __ldg(p.doc_ids + q) == __ldg(p.doc_ids + kv);
+    if ((t & kMaskHash) && ok) ok = hash_mask_eval(p.hash_seed, p.hash_density, b, h, q, kv);
+    return ok;
   }
 };
 

@@ -30,3 +30,12 @@ def dev():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="session")
+def ref_lib():
+    """The reference compiled from its sources (oracle/_ref); skip where it was not built."""
+    import pyoracle
+    if not pyoracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    return pyoracle.ref()

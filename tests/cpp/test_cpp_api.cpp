@@ -61,6 +61,41 @@ int main() {
     HostBlockMask ht = to_host(t);
     EXPECT(ht.full_num[0] == 7 && ht.partial_num[7] == 1);
   }
+  // ---- neighbourhood attention + pixel reorderings: the reference's block-count KATs ---------
+  // (test_block_mask.cpp:267-309): 32x32 canvas, kernel 5, block size 32 and 16
+  {
+    const NAGeometry g(32, 32, 5);
+    auto computed = [](const BlockMask& bm) {
+      HostBlockMask h = to_host(bm);
+      long n = 0;
+      for (auto x : h.full_num) n += x;
+      for (auto x : h.partial_num) n += x;
+      return n;
+    };
+    const i64 n = g.tokens();
+    EXPECT(computed(create_block_mask(na_naive(g), 1, 1, n, n, 32, 32)) == 154);
+    EXPECT(computed(create_block_mask(remap_mask(na_naive(g), tile_permutation(g, 2)), 1, 1, n, n, 32, 32)) == 184);
+    EXPECT(computed(create_block_mask(remap_mask(na_naive(g), morton_permutation(g)), 1, 1, n, n, 32, 32)) == 220);
+    EXPECT(computed(create_block_mask(remap_mask(na_naive(g), tile_permutation(g, 2)), 1, 1, n, n, 16, 16)) == 460);
+    // or_mask: sliding window OR prefix (bit-exact vs the oracle port)
+    BlockMask bo = create_block_mask(or_mask(sliding_window(100), prefix_lm(300)), 1, 1, 1000, 1000, 64, 64);
+    HostBlockMask ho = to_host(bo);
+    fo_mask om{};
+    om.terms = 2;
+    om.or_terms = 8;
+    om.window = 100;
+    om.prefix = 300;
+    std::vector<int64_t> pn(16), pi(256), fn(16), fi(256);
+    EXPECT(fo_create_block_mask(&om, 1, 1, 1000, 1000, 64, 64, pn.data(), pi.data(), fn.data(), fi.data()) == 0);
+    EXPECT(ho.partial_num == pn && ho.partial_idx == pi && ho.full_num == fn && ho.full_idx == fi);
+    bool threw = false;
+    try {
+      NAGeometry bad(8, 8, 4);
+    } catch (const GeometryMismatch&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
   // ---- forward + backward vs the oracle, sliding window + ALiBi, bf16 tcgen05 path ----------
   {
     const i64 B = 1, H = 2, L = 384, D = 128;

@@ -41,6 +41,28 @@ def mask_pair(name: str, L: int = 0, offset: int = 0):
         return fa.hash_mask(seed, dens), O.Mask(terms=O.MASK_HASH, hash_seed=seed, hash_density=dens)
     if name == "never":
         return fa.never_mask(), O.Mask(terms=O.MASK_NEVER)
+    if name.startswith("na"):
+        # na:H:W:K[:tile:T | :morton] — neighbourhood attention on an H x W canvas (L = H*W)
+        parts = name.split(":")
+        h, w, k = int(parts[1]), int(parts[2]), int(parts[3])
+        g = fa.NAGeometry(h, w, k)
+        fm, om = fa.na_naive(g), O.na_naive(h, w, k)
+        if len(parts) > 4:
+            perm = fa.tile_permutation(g, int(parts[5])) if parts[4] == "tile" else fa.morton_permutation(g)
+            fm = fa.remap_mask(fm, perm)
+            om = O.Mask(**{**om.__dict__, "remap": np.asarray(perm, dtype=np.int64)})
+        return fm, om
+    if name.startswith("or_"):
+        # or_sliding_prefix:W:P  /  or_causal_hash:S:D
+        parts = name.split(":")
+        if parts[0] == "or_sliding_prefix":
+            w, p = int(parts[1]), int(parts[2])
+            return (fa.or_mask(fa.sliding_window(w), fa.prefix_lm(p)),
+                    O.Mask(terms=O.MASK_SLIDING, or_terms=O.MASK_PREFIX, window=w, prefix=p))
+        if parts[0] == "or_causal_hash":
+            seed, dens = int(parts[1]), int(parts[2])
+            return (fa.or_mask(fa.causal(), fa.hash_mask(seed, dens)),
+                    O.Mask(terms=O.MASK_CAUSAL, or_terms=O.MASK_HASH, hash_seed=seed, hash_density=dens))
     raise KeyError(name)
 
 

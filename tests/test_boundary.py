@@ -60,7 +60,7 @@ def test_status_names():
     lib = _lib.load()
     names = {i: lib.fa_status_name(i).decode() for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 100, 101)}
     assert names[1] == "ShapeMismatch" and names[6] == "BlockMaskMismatch" and names[10] == "UnmappedBlock"
-    assert lib.fa_abi_version() == 1
+    assert lib.fa_abi_version() == 2  # v2: fa_mask_desc or_terms / natten / remap
 
 
 def test_geometry_validation():

@@ -158,6 +158,44 @@ def morton_permutation_np(n_side: int) -> np.ndarray:
     return out
 
 
+def ref_save_block_mask(mask: Mask, bd, hd, ql, kl, bsq, bskv, path: str):
+    lib = ref()
+    mc = mask.c()
+    _check(lib.ref_save_block_mask(C.byref(mc), *_i64(bd, hd, ql, kl, bsq, bskv), path.encode()), lib)
+
+
+def ref_load_block_mask(path: str, cap_rows: int = 1 << 16, cap_cells: int = 1 << 22):
+    """(header[8], partial_num, partial_idx, full_num, full_idx) as read by the reference."""
+    lib = ref()
+    hdr = np.zeros(8, np.int64)
+    pn, fn = np.zeros(cap_rows, np.int64), np.zeros(cap_rows, np.int64)
+    pi, fi = np.zeros(cap_cells, np.int64), np.zeros(cap_cells, np.int64)
+    _check(lib.ref_load_block_mask(path.encode(), *[_p(a, C.c_int64) for a in (hdr, pn, pi, fn, fi)],
+                                   C.c_int64(cap_rows), C.c_int64(cap_cells)), lib)
+    n = int(hdr[0] * hdr[1])
+    rows, cols = int(hdr[2]), int(hdr[3])
+    return hdr, pn[:n * rows], pi[:n * rows * cols], fn[:n * rows], fi[:n * rows * cols]
+
+
+def ref_write_ppm(mask: Mask, ql, kl, bs, path: str):
+    lib = ref()
+    mc = mask.c()
+    _check(lib.ref_write_ppm(C.byref(mc), *_i64(ql, kl, bs), path.encode()), lib)
+
+
+def ref_save_tensor_f32(x: np.ndarray, path: str):
+    lib = ref()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    _check(lib.ref_save_tensor_f32(_p(x, C.c_float), *_i64(*x.shape), path.encode()), lib)
+
+
+def ref_load_tensor_f32(path: str, shape) -> np.ndarray:
+    lib = ref()
+    out = np.zeros(int(np.prod(shape)), np.float32)
+    _check(lib.ref_load_tensor_f32(path.encode(), _p(out, C.c_float), C.c_int64(out.size)), lib)
+    return out.reshape(shape)
+
+
 def ref_tile_permutation(h: int, w: int, kernel: int, tile: int) -> np.ndarray:
     lib = ref()
     out = np.zeros(h * w, dtype=np.int64)

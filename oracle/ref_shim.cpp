@@ -190,6 +190,62 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// save_block_mask / render_ppm / save_tensor of the reference, for byte-level comparisons
+int ref_save_block_mask(const RefMask* m, int64_t bd, int64_t hd, int64_t ql, int64_t kl, int64_t bsq,
+                        int64_t bskv, const char* path) {
+  try {
+    save_block_mask(path, create_block_mask(make_mask(*m), bd, hd, ql, kl, bsq, bskv));
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+// load a BlockMask file with the reference and return its kv-side arrays (sizes from the header)
+int ref_load_block_mask(const char* path, int64_t* hdr8, int64_t* pn, int64_t* pi, int64_t* fn,
+                        int64_t* fi, int64_t cap_rows, int64_t cap_cells) {
+  try {
+    const BlockMask bm = load_block_mask(path);
+    const int64_t v[8] = {bm.b_dims, bm.h_dims, bm.rows, bm.cols, bm.bs_q, bm.bs_kv, bm.q_len, bm.kv_len};
+    std::copy(v, v + 8, hdr8);
+    if (static_cast<int64_t>(bm.partial_num.size()) > cap_rows ||
+        static_cast<int64_t>(bm.partial_idx.size()) > cap_cells)
+      return 1;
+    std::copy(bm.partial_num.begin(), bm.partial_num.end(), pn);
+    std::copy(bm.partial_idx.begin(), bm.partial_idx.end(), pi);
+    std::copy(bm.full_num.begin(), bm.full_num.end(), fn);
+    std::copy(bm.full_idx.begin(), bm.full_idx.end(), fi);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+int ref_write_ppm(const RefMask* m, int64_t ql, int64_t kl, int64_t bs, const char* path) {
+  try {
+    write_ppm(path, create_block_mask(make_mask(*m), 1, 1, ql, kl, bs, bs), 0, 0);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+int ref_save_tensor_f32(const float* x, int64_t B, int64_t H, int64_t L, int64_t D, const char* path) {
+  try {
+    save_tensor(path, Tensor4<float>(B, H, L, D, std::vector<float>(x, x + B * H * L * D)));
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+int ref_load_tensor_f32(const char* path, float* out, int64_t cap) {
+  try {
+    const auto t = load_tensor<float>(path);
+    if (static_cast<int64_t>(t.data().size()) > cap) return 1;
+    std::copy(t.data().begin(), t.data().end(), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 // tile_permutation / morton_permutation (mask_library.cpp:164-201): forward table into out[h*w]
 int ref_tile_permutation(int64_t h, int64_t w, int64_t k, int64_t tile, int64_t* out) {
   try {

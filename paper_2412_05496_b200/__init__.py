@@ -11,5 +11,8 @@ from .api import *  # noqa: E402,F401,F403
 from .api import (AttentionConfig, AttentionOutput, BlockMask, Gradients, PagedKVCache,  # noqa: E402,F401
                   PageTable, backward, convert_block_mask, create_block_mask, decode, flex_attention,
                   forward, random_tensor, sparsity, transpose)
+from .fixtures import (KIND_EMPTY, KIND_FULL, KIND_PARTIAL, block_mask_from_grid,  # noqa: E402,F401
+                       demote_full_to_partial, load_block_mask, load_tensor, promote_empty_to_partial,
+                       render_ascii, render_ppm, save_block_mask, save_tensor, to_dense, write_ppm)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

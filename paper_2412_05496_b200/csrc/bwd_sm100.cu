@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.q_full[qst], (blk >> 1) & 1);  // cterm of this q block
         tc_fence_after();
         if (threadIdx.x == 0) trace_ev(p, blk, 0);
-        uint32_t pgp[32];  // P·scale·mod'(s) as packed bf16 pairs, kept for phase B
+        float pg[64];  // P·scale·mod'(s), kept in fp32 for phase B
         {
           uint32_t sr[64];
           tmem_ld32(tm + kS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
@@ -545,13 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               pp[2 * i4] = pack_bf16(pv[0], pv[1]);
               pp[2 * i4 + 1] = pack_bf16(pv[2], pv[3]);
-              if constexpr (ScoreT::kUnitGrad) {
-                pgp[2 * i4] = pp[2 * i4];
-                pgp[2 * i4 + 1] = pp[2 * i4 + 1];
-              } else {
-                pgp[2 * i4] = pack_bf16(pv[0] * gv[0], pv[1] * gv[1]);
-                pgp[2 * i4 + 1] = pack_bf16(pv[2] * gv[2], pv[3] * gv[3]);
-              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pg[i4 * 4 + e] = ScoreT::kUnitGrad ? pv[e] : pv[e] * gv[e];
             }
           };
           if (full) body(std::false_type{});
@@ -569,38 +564,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (threadIdx.x == 0) trace_ev(p, blk, 2);
         {
-          uint32_t dpr[64];
-          tmem_ld32(tm + kDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&dpr[0]));
-          tmem_ld32(tm + kDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&dpr[32]));
           const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[ds_] + wg * 64);
           // the previous block's dQ must have read the dS^T smem buffer
           mbar_wait(&sm.ds_free, (blk & 1) ^ 1);
           uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
+          uint32_t dpr[2][32];
+          tmem_ld32(tm + kDP + wg * 64, dpr[0]);
           tmem_wait_ld();
-          uint32_t dsp[32];
+          tmem_ld32(tm + kDP + wg * 64 + 32, dpr[1]);  // overlaps the first half's math
 #pragma unroll
-          for (int i4 = 0; i4 < 16; ++i4) {
-            const float4 d4 = dlt4[i4];
-            const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-            float a[4];
+          for (int hh = 0; hh < 2; ++hh) {
+            if (hh == 1) tmem_wait_ld();
+            uint32_t dsp[16];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int ii = i4 * 4 + e;
-              const uint32_t w = pgp[ii >> 1];
-              const float pg = __uint_as_float((ii & 1) ? (w & 0xffff0000u) : (w << 16));
-              a[e] = pg * (__uint_as_float(dpr[ii]) - dv4[e]);
+            for (int i4 = 0; i4 < 8; ++i4) {
+              const float4 d4 = dlt4[hh * 8 + i4];
+              const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+              float a[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                a[e] = pg[hh * 32 + i4 * 4 + e] * (__uint_as_float(dpr[hh][i4 * 4 + e]) - dv4[e]);
+              dsp[2 * i4] = pack_bf16(a[0], a[1]);
+              dsp[2 * i4 + 1] = pack_bf16(a[2], a[3]);
             }
-            dsp[2 * i4] = pack_bf16(a[0], a[1]);
-            dsp[2 * i4 + 1] = pack_bf16(a[2], a[3]);
-          }
-          // dS^T (bf16) over dP^T columns already read: the A operand of dK (TS)
-          tmem_st32(tm + kDP + wg * 64, dsp);
-          // dS^T row j (the MN-major operand of dQ): 16-byte units 0..7 of this warpgroup's
-          // 64-wide q chunk, 128-byte swizzle
+            // dS^T (bf16) over dP^T columns already read: the A operand of dK (TS)
+            tmem_st16(tm + kDP + wg * 64 + hh * 16, dsp);
+            // dS^T row j (the MN-major operand of dQ): 16-byte units 4hh..4hh+3 of this
+            // warpgroup's 64-wide q chunk, 128-byte swizzle
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            *reinterpret_cast<uint4*>(ds_row + ((u ^ (j & 7)) << 4)) =
-                make_uint4(dsp[4 * u], dsp[4 * u + 1], dsp[4 * u + 2], dsp[4 * u + 3]);
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<uint4*>(ds_row + (((hh * 4 + u) ^ (j & 7)) << 4)) =
+                  make_uint4(dsp[4 * u], dsp[4 * u + 1], dsp[4 * u + 2], dsp[4 * u + 3]);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.do_free[ds_]);

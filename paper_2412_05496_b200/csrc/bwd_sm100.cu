@@ -499,7 +499,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           uint32_t sr[64];
           tmem_ld32(tm + kS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-          tmem_ld32(tm + kS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           // mask bits for this kv row over the 64 q columns (bounds folded in)
           uint32_t bits0 = 0u, bits1 = 0u;
           if (!full && kv_in) {
@@ -512,11 +511,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (ScoreT::kKind == 1)
             rowc = colc.step * static_cast<float>(r * kTile + score.p.q_offset - kv);
           tmem_wait_ld();
+          // the second half of S^T loads while the first half is exponentiated
+          tmem_ld32(tm + kS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           uint32_t pp[32];
           // full blocks skip mask_mod entirely (no per-score select)
           auto body = [&](auto masked) {
 #pragma unroll
             for (int i4 = 0; i4 < 16; ++i4) {
+              if (i4 == 8) tmem_wait_ld();
               const float4 c4 = ct4[i4];
               const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
               float pv[4], gv[4];

@@ -301,7 +301,8 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
   fa_status s;
   if ((s = check_qkv(a->q, a->k_cache, a->v_cache, a->gqa_group))) return s;
   if ((s = check_tensor(a->out, "out"))) return s;
-  FA_REQUIRE(a->q.dtype == FA_BF16, FA_UNSUPPORTED, "decode: bf16 only");
+  FA_REQUIRE(a->q.dtype == FA_BF16 || a->pt == nullptr, FA_UNSUPPORTED,
+             "decode: a paged cache needs bf16 (float32 decode is unpaged)");
   const int64_t n_new = a->q.l;
   int64_t logical_kv = a->k_cache.l;
   if (a->pt != nullptr) {
@@ -334,6 +335,14 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
   if (m.terms & kMaskDocument)
     FA_REQUIRE(m.doc_len >= logical_kv, FA_INDEX_OUT_OF_RANGE,
                "document_mask: token index outside id table");
+  if (a->q.dtype == FA_F32) {
+    // decode<float> is forward_impl over the shifted mask (engine.cpp:403-427): the fp32
+    // CUDA-core forward with q_offset applied to the mask and score terms
+    const AttnGeom ga = geom_of(a->q, a->k_cache, a->bm, a->scale, a->gqa_group);
+    return launch_fwd_simt(ga, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse, FA_F32,
+                           kv_view(a->bm), to_mask_params(m), mask_kind_of(m), to_score_params(sc),
+                           (int)sc.terms, static_cast<cudaStream_t>(stream));
+  }
   DecodeGeom g{};
   g.a = geom_of(a->q, a->k_cache, a->bm, a->scale, a->gqa_group);
   g.logical_kv = (int)(a->pt ? logical_kv : a->k_cache.l);

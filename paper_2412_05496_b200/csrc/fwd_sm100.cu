@@ -81,10 +81,10 @@ struct FwdParams {
 #ifndef FA_FWD_TRACE_BUILD
 #define FA_FWD_TRACE_BUILD 0
 #endif
-constexpr int kFTraceSteps = 512, kFTraceEv = 8;
+constexpr int kFTraceSteps = 512, kFTraceEv = 16;
 __device__ __forceinline__ void ftrace(const FwdParams& p, int step, int ev) {
   if constexpr (FA_FWD_TRACE_BUILD != 0) {
-    if (p.trace != nullptr && blockIdx.x == 0 && step < kFTraceSteps) {
+    if (p.trace != nullptr && blockIdx.x == 0 && step < kFTraceSteps && (threadIdx.x & 31) == 0) {
       long long t;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
       p.trace[step * kFTraceEv + ev] = t;
@@ -109,7 +109,8 @@ struct alignas(1024) Smem {
   int32_t ulen[2];
   int32_t uitem[2];   // work item of the buffer, -1 = no more work
   uint64_t q_full[2], q_free[2];
-  uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages], kv_empty[Cfg<D>::kStages];
+  uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages];
+  uint64_t k_empty[Cfg<D>::kStages], v_empty[Cfg<D>::kStages];  // released separately
   uint64_t s_full[2], p_full[2][2], o_full[2];  // p_full[tile][half of the kv block]
   uint64_t item_full[2], item_empty[2];
   uint32_t tmem_base;
@@ -158,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.v_full[s], 1);
-      mbar_init(&sm.kv_empty[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+      mbar_init(&sm.v_empty[s], 1);
     }
     fence_barrier_init();
   }
@@ -247,20 +249,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb = p.Bkv == 1 ? 0 : it.b, kh = it.h / p.G;
         for (int j = 0; j < len; ++j, ++kv_it) {
           const int st = kv_it % C::kStages;
-          mbar_wait(&sm.kv_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          // K_j's slot frees when the QKs of block j-2 complete (an iteration before V's)
           const int colb = static_cast<int>(static_cast<uint32_t>(sm.ulist[buf][j]) & kColMask);
+          mbar_wait(&sm.k_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          ftrace(p, kv_it, 12);
           mbar_expect_tx(&sm.k_full[st], C::kTileBytes);
           for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.k[st] + ch * C::kChunkBytes, &tmK, &sm.k_full[st], ch * 64,
                         colb * kTile, kb * p.Hkv + kh);
+          mbar_wait(&sm.v_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          ftrace(p, kv_it, 13);
           mbar_expect_tx(&sm.v_full[st], C::kTileBytes);
           for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.v[st] + ch * C::kChunkBytes, &tmV, &sm.v_full[st], ch * 64,
                         colb * kTile, kb * p.Hkv + kh);
         }
       }
-    } else if (warp == 9 && lane == 0) {
+    } else if (warp == 9) {
       // ===================== MMA issuer =====================
+      // The whole warp runs the (warp-uniform) control flow and one elected lane issues:
+      // descriptors then live in uniform registers and each tcgen05.mma is one UTCHMMA
+      // (a lane-0-only branch makes ptxas wrap every MMA in an ELECT/R2UR waterfall loop).
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
       const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
@@ -270,38 +280,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n = 0;
       // descriptors rebuilt per GEMM from an opaque base (+ K-step offsets in the address
       // field): ptxas would otherwise hoist them all out of the loop and spill
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
+        __syncwarp();
+      };
       auto issue_qk = [&](int t, int st) {
-        const uint64_t a0 = make_sdesc_sw128(opaque_u32(q_addr[t]), 16, 1024);
-        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.k[st])), 16, 1024);
+        if (elect_one()) {
+          const uint64_t a0 = make_sdesc_sw128(q_addr[t], 16, 1024);
+          const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.k[st]), 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
-          umma_ss(tmem + t * 128, a0 + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
+            umma_ss(tm + t * 128, a0 + off, b0 + off, idesc_qk, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full[t]);
         }
-        umma_commit(&sm.s_full[t]);
+        __syncwarp();
       };
       // O_t += P_t V: the first 64 kv (P columns 0-31) as soon as the softmax released them,
       // the rest when the second half of P is in TMEM
       constexpr bool kSplitP = !ScoreT::kUnitGrad;  // see the softmax
       auto issue_pv = [&](int t, int st, bool acc, uint32_t ph) {
-        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.v[st])), C::kChunkBytes, 1024);
+        const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.v[st]), C::kChunkBytes, 1024);
         if constexpr (kSplitP) {
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             mbar_wait(&sm.p_full[t][hf], ph);
             tc_fence_after();
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = hf * 4; kk < hf * 4 + 4; ++kk)
-              umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
-                      (acc || kk > 0) ? 1u : 0u);
+              for (int kk = hf * 4; kk < hf * 4 + 4; ++kk)
+                umma_ts(tm + 256 + t * D, tm + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
+                        (acc || kk > 0) ? 1u : 0u);
+            }
+            __syncwarp();
           }
         } else {
           mbar_wait(&sm.p_full[t][1], ph);
           tc_fence_after();
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk)
-            umma_ts(tmem + 256 + t * D, tmem + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
-                    (acc || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < kTile / 16; ++kk)
+              umma_ts(tm + 256 + t * D, tm + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
+                      (acc || kk > 0) ? 1u : 0u);
+          }
+          __syncwarp();
         }
       };
       for (;; ++n) {
@@ -321,15 +344,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int t = 0; t < 2; ++t)
-          if (last_qk[t] < 0) umma_commit(&sm.q_free[t]);
+          if (last_qk[t] < 0) commit(&sm.q_free[t]);
         bool first_pv[2] = {true, true};
         if (len > 0) {
           const int st0 = kv_it % C::kStages;
           mbar_wait(&sm.k_full[st0], (kv_it / C::kStages) & 1);
           tc_fence_after();
           const uint32_t e0 = U[0];
-          if (e0 & kIn0) { issue_qk(0, st0); if (last_qk[0] == 0) umma_commit(&sm.q_free[0]); }
-          if (e0 & kIn1) { issue_qk(1, st0); if (last_qk[1] == 0) umma_commit(&sm.q_free[1]); }
+          if (e0 & kIn0) { issue_qk(0, st0); if (last_qk[0] == 0) commit(&sm.q_free[0]); }
+          if (e0 & kIn1) { issue_qk(1, st0); if (last_qk[1] == 0) commit(&sm.q_free[1]); }
+          commit(&sm.k_empty[st0]);
         }
         for (int j = 0; j < len; ++j) {
           const int it_j = kv_it + j;
@@ -338,7 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t en = (j + 1 < len) ? U[j + 1] : 0u;
           const int st1 = (it_j + 1) % C::kStages;
           bool k1_ready = false;
+          ftrace(p, it_j, 15);
           mbar_wait(&sm.v_full[st], (it_j / C::kStages) & 1);
+          ftrace(p, it_j, 14);
           tc_fence_after();
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
@@ -346,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (e & in_bit) {
               ftrace(p, mg[t], 4 + t);
               issue_pv(t, st, !first_pv[t], p_phase[t]);
+              ftrace(p, mg[t], 8 + t);
               p_phase[t] ^= 1;
               first_pv[t] = false;
               ++mg[t];
@@ -356,16 +383,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 k1_ready = true;
               }
+              ftrace(p, mg[t], 10 + t);
               issue_qk(t, st1);
               ftrace(p, mg[t], 6 + t);
-              if (last_qk[t] == j + 1) umma_commit(&sm.q_free[t]);
+              if (last_qk[t] == j + 1) commit(&sm.q_free[t]);
             }
           }
-          umma_commit(&sm.kv_empty[st]);
+          if (k1_ready) commit(&sm.k_empty[st1]);
+          commit(&sm.v_empty[st]);
         }
         kv_it += len;
-        for (int t = 0; t < 2; ++t) umma_commit(&sm.o_full[t]);
-        mbar_arrive(&sm.item_empty[buf]);
+        for (int t = 0; t < 2; ++t) commit(&sm.o_full[t]);
+        if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
       }
     }
     FA_FWD_TEARDOWN();
@@ -644,8 +673,14 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
     const long long t0 = h[20 * kFTraceEv];
     for (int s = 20; s < 28; ++s) {
       const long long* e = h + s * kFTraceEv;
-      fprintf(stderr, "[fwd trace] step %d: S0seen %lld P0done %lld PV0 %lld QK0next %lld | S1seen %lld P1done %lld PV1 %lld QK1next %lld\n",
-              s, e[0] - t0, e[1] - t0, e[4] - t0, e[6] - t0, e[2] - t0, e[3] - t0, e[5] - t0, e[7] - t0);
+      fprintf(stderr, "[fwd trace] step %d: S0seen %lld P0done %lld PV0 %lld..%lld QK0 %lld..%lld | S1seen %lld P1done %lld PV1 %lld..%lld QK1 %lld..%lld\n",
+              s, e[0] - t0, e[1] - t0, e[4] - t0, e[8] - t0, e[10] - t0, e[6] - t0, e[2] - t0, e[3] - t0,
+              e[5] - t0, e[9] - t0, e[11] - t0, e[7] - t0);
+    }
+    for (int s = 20; s < 28; ++s) {
+      const long long* e = h + s * kFTraceEv;
+      fprintf(stderr, "[fwd trace] block %d: K issued %lld  V issued %lld  MMA wants V %lld  V seen %lld\n", s,
+              e[12] - t0, e[13] - t0, e[15] - t0, e[14] - t0);
     }
     double sm0 = 0, per = 0;
     int cnt = 0;

@@ -86,7 +86,7 @@ struct BwdParams {
 constexpr int kTraceTasks = 256, kTraceEv = 24;
 __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
   if constexpr (FA_BWD_TRACE_BUILD != 0) {
-    if (p.trace != nullptr && blockIdx.x == 0 && task < kTraceTasks) {
+    if (p.trace != nullptr && blockIdx.x == 0 && task < kTraceTasks && (threadIdx.x & 31) == 0) {
       long long t;
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
       p.trace[task * kTraceEv + ev] = t;
@@ -333,24 +333,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     FA_BWD_TEARDOWN();
   } else if (warp == 13) {
-    if (lane == 0) {
+    {
       // ===================== MMA issuer =====================
+      // The whole warp runs the warp-uniform control flow and one elected lane issues, so
+      // descriptors sit in uniform registers (a lane-0-only branch costs an ELECT/R2UR
+      // waterfall loop around every tcgen05.mma).
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
+        __syncwarp();
+      };
       constexpr uint32_t idesc_ss = make_idesc_bf16(128, 128, 0, 0);   // S^T, dP^T
       constexpr uint32_t idesc_kn = make_idesc_bf16(128, D, 0, 1);     // dV (TS), dK (SS)
       constexpr uint32_t idesc_mm = make_idesc_bf16(128, D, 1, 1);     // dQ = dS K (D = 64)
       constexpr uint32_t idesc_mmT = make_idesc_bf16(D, 128, 1, 1);    // dQ^T = K^T dS^T (D = 128)
       const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v), ds_addr = smem_u32(sm.ds);
-      // Descriptors are rebuilt from an opaque base per GEMM (+ the K-step offset in the
-      // 14-bit address field) so ptxas does not hoist ~100 loop-invariant descriptor
-      // registers out of the persistent loop (they spill and every issue then waits on LDL).
-      auto mma_kmajor = [&](uint32_t d_col, uint32_t a_addr, uint32_t b_addr) {
-        const uint64_t a0 = make_sdesc_sw128(opaque_u32(a_addr), 16, 1024);
-        const uint64_t b0 = make_sdesc_sw128(opaque_u32(b_addr), 16, 1024);
+      // issue + commit in one elected region
+      auto mma_kmajor = [&](uint32_t d_col, uint32_t a_addr, uint32_t b_addr, uint64_t* bar) {
+        if (elect_one()) {
+          const uint64_t a0 = make_sdesc_sw128(a_addr, 16, 1024);
+          const uint64_t b0 = make_sdesc_sw128(b_addr, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
-          umma_ss(tmem + d_col, a0 + off, b0 + off, idesc_ss, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * C::kChunkBytes + (kk & 3) * 32) >> 4;
+            umma_ss(tm + d_col, a0 + off, b0 + off, idesc_ss, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(bar);
         }
+        __syncwarp();
       };
       auto issue_s = [&](int b) {  // S^T(b) = K Q(b)^T
         const int st = b & 1;
@@ -358,8 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.q_full[st], (b >> 1) & 1);
         trace_ev(p, b, 13);
         tc_fence_after();
-        mma_kmajor(kS, k_addr, smem_u32(sm.q[st]));
-        umma_commit(&sm.s_full);
+        mma_kmajor(kS, k_addr, smem_u32(sm.q[st]), &sm.s_full);
         trace_ev(p, b, 4);
       };
       auto issue_dp = [&](int b) {  // dP^T(b) = V dO(b)^T, after dQ(b-1) left TMEM
@@ -370,8 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.dq_empty, (b & 1) ^ 1);
         trace_ev(p, b, 16);
         tc_fence_after();
-        mma_kmajor(kDP, v_addr, smem_u32(sm.dO[ds_]));
-        umma_commit(&sm.dp_full);
+        mma_kmajor(kDP, v_addr, smem_u32(sm.dO[ds_]), &sm.dp_full);
         trace_ev(p, b, 6);
       };
       auto issue_dv = [&](int b, bool acc) {  // dV += P^T(b) dO(b)   (TS)
@@ -380,43 +388,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&sm.p_full, b & 1);
         trace_ev(p, b, 18);
         tc_fence_after();
-        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.dO[ds_])), C::kChunkBytes, 1024);
+        if (elect_one()) {
+          const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.dO[ds_]), C::kChunkBytes, 1024);
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk) {
-          const uint32_t a_col = kS + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
-          umma_ts(tmem + kDV, tmem + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kTile / 16; ++kk) {
+            const uint32_t a_col = kS + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
+            umma_ts(tm + kDV, tm + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&sm.do_free[ds_]);
         }
-        umma_commit(&sm.do_free[ds_]);
+        __syncwarp();
       };
       auto issue_dq = [&](int b) {  // dQ(b) over the dP columns, after dK(b) read dS^T there
         trace_ev(p, b, 19);
-        const uint64_t k0 = make_sdesc_sw128(opaque_u32(k_addr), C::kChunkBytes, 1024);
-        const uint64_t s0 = make_sdesc_sw128(opaque_u32(ds_addr), kTile * 128, 1024);
-        if constexpr (D == 128) {
-          // dQ^T = K^T dS^T (M = head dim, N = q): the reduction warps own one head-dim
-          // index per lane and add whole 128-byte lines
+        if (elect_one()) {
+          const uint64_t k0 = make_sdesc_sw128(k_addr, C::kChunkBytes, 1024);
+          const uint64_t s0 = make_sdesc_sw128(ds_addr, kTile * 128, 1024);
+          if constexpr (D == 128) {
+            // dQ^T = K^T dS^T (M = head dim, N = q): the reduction warps own one head-dim
+            // index per lane and add whole 128-byte lines
 #pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk)
-            umma_ss(tmem + kDP, k0 + kk * (2048 >> 4), s0 + kk * (2048 >> 4), idesc_mmT, kk > 0 ? 1u : 0u);
-        } else {
+            for (int kk = 0; kk < kTile / 16; ++kk)
+              umma_ss(tm + kDP, k0 + kk * (2048 >> 4), s0 + kk * (2048 >> 4), idesc_mmT, kk > 0 ? 1u : 0u);
+          } else {
 #pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk)
-            umma_ss(tmem + kDP, s0 + kk * (2048 >> 4), k0 + kk * (2048 >> 4), idesc_mm, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < kTile / 16; ++kk)
+              umma_ss(tm + kDP, s0 + kk * (2048 >> 4), k0 + kk * (2048 >> 4), idesc_mm, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.dq_full);
+          umma_commit(&sm.ds_free);
         }
-        umma_commit(&sm.dq_full);
-        umma_commit(&sm.ds_free);
+        __syncwarp();
       };
       auto issue_dk = [&](int b, bool acc) {  // dK += dS^T(b) Q(b)   (TS: dS^T from TMEM)
         mbar_wait(&sm.ds_full, b & 1);
         tc_fence_after();
         trace_ev(p, b, 5);
-        const uint64_t b0 = make_sdesc_sw128(opaque_u32(smem_u32(sm.q[b & 1])), C::kChunkBytes, 1024);
+        if (elect_one()) {
+          const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.q[b & 1]), C::kChunkBytes, 1024);
 #pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk) {
-          const uint32_t a_col = kDP + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
-          umma_ts(tmem + kDK, tmem + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kTile / 16; ++kk) {
+            const uint32_t a_col = kDP + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8);
+            umma_ts(tm + kDK, tm + a_col, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&sm.q_free[b & 1]);
         }
-        umma_commit(&sm.q_free[b & 1]);
+        __syncwarp();
         trace_ev(p, b, 20);
       };
       int blk = 0;
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = n & 1;
         mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
         const int item = sm.uitem[buf];
-        mbar_arrive(&sm.item_empty[buf]);
+        if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
         if (item < 0) break;
         const KvItem it = decode_kv_item(p, item);
         const int T = count_tasks(p, it);
@@ -432,9 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (T == 0) {
           mbar_wait(&sm.dkdv_free, (n & 1) ^ 1);
           mbar_wait(&sm.v_full, n & 1);
-          umma_commit(&sm.dkdv_full);
-          umma_commit(&sm.k_free);
-          umma_commit(&sm.v_free);
+          commit(&sm.dkdv_full);
+          commit(&sm.k_free);
+          commit(&sm.v_free);
           continue;
         }
         issue_s(blk);
@@ -447,16 +464,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (t + 1 < T) issue_s(b + 1);
           issue_dk(b, t > 0);
           issue_dq(b);
-          if (t + 1 == T) umma_commit(&sm.k_free);  // K's last reader was dQ(T-1)
+          if (t + 1 == T) commit(&sm.k_free);  // K's last reader was dQ(T-1)
           if (t + 1 < T) {
             issue_dp(b + 1);
-            if (t + 2 == T) umma_commit(&sm.v_free);  // V's last reader was dP(T-1)
+            if (t + 2 == T) commit(&sm.v_free);  // V's last reader was dP(T-1)
             issue_dv(b + 1, true);
           } else if (T == 1) {
-            umma_commit(&sm.v_free);
+            commit(&sm.v_free);
           }
         }
-        umma_commit(&sm.dkdv_full);
+        commit(&sm.dkdv_full);
         blk += T;
       }
     }

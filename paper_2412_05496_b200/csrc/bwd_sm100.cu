@@ -94,6 +94,10 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
   }
 }
 
+#ifndef FA_BWD_DKSS
+#define FA_BWD_DKSS 1  // dK as an SS MMA from the dS^T smem buffer, issued after dQ
+#endif
+constexpr bool kDkSS = FA_BWD_DKSS != 0;
 #ifndef FA_BWD_DQ_TMA
 #define FA_BWD_DQ_TMA 1
 #endif
@@ -118,7 +122,7 @@ struct alignas(1024) BSmem {
   uint8_t dO[BCfg<D>::kDoStages][BCfg<D>::kTileBytes];
   uint8_t ds[kTile * kTile * 2];  // dS^T [kv][q], SW128, two 64-wide q chunks
   float lse2[2][kTile];
-  float delta[BCfg<D>::kDoStages][kTile];
+  float delta[2][kTile];  // Δ rides with the q stage (q_full), so dO frees after dV alone
   float dq_stage[4][2][BCfg<D>::kStageFloats];  // per reduction warp, double-buffered
   uint64_t k_full, v_full, k_free, v_free;
   uint64_t q_full[2], q_free[2];
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < C::kDoStages; ++s) {
       mbar_init(&sm.do_full[s], 1);
-      mbar_init(&sm.do_free[s], 1 + 8);  // dV MMA commit + the 8 compute warps (Δ read)
+      mbar_init(&sm.do_free[s], 1);  // the dV MMA commit
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.p_full, 8);
@@ -302,11 +306,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long row0 = static_cast<long long>(b * p.Hq + h) * p.Lq_pad + r * kTile;
           mbar_wait(&sm.q_free[st], ((blk >> 1) & 1) ^ 1);
           trace_ev(p, blk, 10);
-          mbar_expect_tx(&sm.q_full[st], C::kTileBytes + kTile * 4);
+          mbar_expect_tx(&sm.q_full[st], C::kTileBytes + 2 * kTile * 4);
           for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.q[st] + ch * C::kChunkBytes, &tmQ, &sm.q_full[st], ch * 64, r * kTile,
                         b * p.Hq + h);
           bulk_load(sm.lse2[st], p.lse2 + row0, kTile * 4, &sm.q_full[st]);
+          bulk_load(sm.delta[st], p.delta + row0, kTile * 4, &sm.q_full[st]);
           if (!v_loaded) {
             mbar_wait(&sm.v_free, (n & 1) ^ 1);
             mbar_expect_tx(&sm.v_full, C::kTileBytes);
@@ -318,11 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ds_ = blk % C::kDoStages;
           mbar_wait(&sm.do_free[ds_], ((blk / C::kDoStages) & 1) ^ 1);
           trace_ev(p, blk, 11);
-          mbar_expect_tx(&sm.do_full[ds_], C::kTileBytes + kTile * 4);
+          mbar_expect_tx(&sm.do_full[ds_], C::kTileBytes);
           for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.dO[ds_] + ch * C::kChunkBytes, &tmDO, &sm.do_full[ds_], ch * 64, r * kTile,
                         b * p.Hq + h);
-          bulk_load(sm.delta[ds_], p.delta + row0, kTile * 4, &sm.do_full[ds_]);
           ++blk;
         }
         if (!v_loaded) {  // an item with no q blocks still owns one V phase
@@ -399,7 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
-      auto issue_dq = [&](int b) {  // dQ(b) over the dP columns, after dK(b) read dS^T there
+      auto issue_dq = [&](int b) {  // dQ(b) over the dP columns (dS^T(b) read from smem)
+        if constexpr (kDkSS) {
+          mbar_wait(&sm.ds_full, b & 1);
+          tc_fence_after();
+          trace_ev(p, b, 5);
+        }
         trace_ev(p, b, 19);
         if (elect_one()) {
           const uint64_t k0 = make_sdesc_sw128(k_addr, C::kChunkBytes, 1024);
@@ -416,11 +425,29 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_ss(tm + kDP, s0 + kk * (2048 >> 4), k0 + kk * (2048 >> 4), idesc_mm, kk > 0 ? 1u : 0u);
           }
           umma_commit(&sm.dq_full);
-          umma_commit(&sm.ds_free);
+          if constexpr (!kDkSS) umma_commit(&sm.ds_free);
         }
         __syncwarp();
       };
-      auto issue_dk = [&](int b, bool acc) {  // dK += dS^T(b) Q(b)   (TS: dS^T from TMEM)
+      auto issue_dk = [&](int b, bool acc) {  // dK += dS^T(b) Q(b)
+        if constexpr (kDkSS) {
+          // SS, dS^T from the smem buffer (K-major, the layout of a TMA tile): dK is off the
+          // B -> dQ -> drain -> dP chain and B stores dS^T to smem only
+          if (elect_one()) {
+            const uint64_t a0 = make_sdesc_sw128(ds_addr, 16, 1024);
+            const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.q[b & 1]), C::kChunkBytes, 1024);
+#pragma unroll
+            for (int kk = 0; kk < kTile / 16; ++kk) {
+              const uint32_t aoff = ((kk >> 2) * (kTile * 128) + (kk & 3) * 32) >> 4;
+              umma_ss(tm + kDK, a0 + aoff, b0 + kk * (2048 >> 4), idesc_kn, (acc || kk > 0) ? 1u : 0u);
+            }
+            umma_commit(&sm.q_free[b & 1]);
+            umma_commit(&sm.ds_free);
+          }
+          __syncwarp();
+          trace_ev(p, b, 20);
+          return;
+        }
         mbar_wait(&sm.ds_full, b & 1);
         tc_fence_after();
         trace_ev(p, b, 5);
@@ -462,8 +489,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < T; ++t) {
           const int b = blk + t;
           if (t + 1 < T) issue_s(b + 1);
-          issue_dk(b, t > 0);
-          issue_dq(b);
+          if constexpr (kDkSS) {
+            issue_dq(b);
+            issue_dk(b, t > 0);
+          } else {
+            issue_dk(b, t > 0);
+            issue_dq(b);
+          }
           if (t + 1 == T) commit(&sm.k_free);  // K's last reader was dQ(T-1)
           if (t + 1 < T) {
             issue_dp(b + 1);
@@ -502,7 +534,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool full;
       while (ti.next(b, h, r, full)) {
         const int qst = blk & 1;
-        const int ds_ = blk % C::kDoStages;
         const int q0 = r * kTile + wg * 64;
         // ---------------- phase A: P^T ----------------
         // The preprocess stored per q column  cterm = log2(scale) - lse·log2e  (+ the q part of
@@ -579,11 +610,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 0) trace_ev(p, blk, 1);
         // ---------------- phase B: dS^T ----------------
         mbar_wait(&sm.dp_full, blk & 1);
-        mbar_wait(&sm.do_full[ds_], (blk / C::kDoStages) & 1);  // Δ of this q block
         tc_fence_after();
         if (threadIdx.x == 0) trace_ev(p, blk, 2);
         {
-          const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[ds_] + wg * 64);
+          const float4* dlt4 = reinterpret_cast<const float4*>(sm.delta[qst] + wg * 64);
           // the previous block's dQ must have read the dS^T smem buffer
           mbar_wait(&sm.ds_free, (blk & 1) ^ 1);
           uint8_t* ds_row = sm.ds + wg * (kTile * 128) + j * 128;
@@ -607,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               dsp[2 * i4 + 1] = pack_bf16(a[2], a[3]);
             }
             // dS^T (bf16) over dP^T columns already read: the A operand of dK (TS)
-            tmem_st16(tm + kDP + wg * 64 + hh * 16, dsp);
+            if constexpr (!kDkSS) tmem_st16(tm + kDP + wg * 64 + hh * 16, dsp);
             // dS^T row j (the MN-major operand of dQ): 16-byte units 4hh..4hh+3 of this
             // warpgroup's 64-wide q chunk, 128-byte swizzle
 #pragma unroll
@@ -616,8 +646,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                   make_uint4(dsp[4 * u], dsp[4 * u + 1], dsp[4 * u + 2], dsp[4 * u + 3]);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.do_free[ds_]);
         fence_proxy_async();
         tmem_wait_st();
         tc_fence_before();

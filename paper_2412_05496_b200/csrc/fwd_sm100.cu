@@ -56,6 +56,14 @@ namespace {
 #ifndef FA_FWD_EMU
 #define FA_FWD_EMU 1  // part of the exponentials on the FMA pipe in full blocks
 #endif
+#ifndef FA_FWD_EMU_EVERY
+#define FA_FWD_EMU_EVERY 4  // one exponential pair in this many is emulated
+#endif
+#ifndef FA_FWD_SPLITP
+#define FA_FWD_SPLITP 0  // 1: every score variant releases P in two halves
+#endif
+template <class ScoreT>
+constexpr bool split_p() { return FA_FWD_SPLITP != 0 || !ScoreT::kUnitGrad; }
 constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, 2 idle) warpgroup
 constexpr int kTile = 128;           // query rows per tile == kv rows per block
 constexpr int kMaxCols = 1024;       // max kv blocks per row (KV_LEN <= 131072)
@@ -81,7 +89,7 @@ struct FwdParams {
 #ifndef FA_FWD_TRACE_BUILD
 #define FA_FWD_TRACE_BUILD 0
 #endif
-constexpr int kFTraceSteps = 512, kFTraceEv = 16;
+constexpr int kFTraceSteps = 512, kFTraceEv = 24;
 __device__ __forceinline__ void ftrace(const FwdParams& p, int step, int ev) {
   if constexpr (FA_FWD_TRACE_BUILD != 0) {
     if (p.trace != nullptr && blockIdx.x == 0 && step < kFTraceSteps && (threadIdx.x & 31) == 0) {
@@ -150,8 +158,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_free[t], 1);
       mbar_init(&sm.s_full[t], 1);
       // split P (soft-capped scores): one arrival per warp and half; else per thread, [1] only
-      mbar_init(&sm.p_full[t][0], ScoreT::kUnitGrad ? 128 : 4);
-      mbar_init(&sm.p_full[t][1], ScoreT::kUnitGrad ? 128 : 4);
+      mbar_init(&sm.p_full[t][0], split_p<ScoreT>() ? 4 : 128);
+      mbar_init(&sm.p_full[t][1], split_p<ScoreT>() ? 4 : 128);
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
@@ -299,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // O_t += P_t V: the first 64 kv (P columns 0-31) as soon as the softmax released them,
       // the rest when the second half of P is in TMEM
-      constexpr bool kSplitP = !ScoreT::kUnitGrad;  // see the softmax
+      constexpr bool kSplitP = split_p<ScoreT>();  // see the softmax
       auto issue_pv = [&](int t, int st, bool acc, uint32_t ph) {
         const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.v[st]), C::kChunkBytes, 1024);
         if constexpr (kSplitP) {
@@ -448,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bits[cc] = qi < p.Lq ? mask.bits32(it.b, it.h, qi, kv0 + cc * 32, p.Lkv) : 0u;
         }
         tmem_wait_ld();
+        if (row == 0) ftrace(p, gs, 16);
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         auto pass1 = [&](auto masked) {
 #pragma unroll
@@ -490,12 +499,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           l *= alpha;
         }
         if (need || m == -INFINITY) m = m_new;
+        if (row == 0) ftrace(p, gs, 17);
         const float msub = (m == -INFINITY) ? 0.f : m;
         // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1).
         // With a soft-capped score (tanh + exp2 per score: the MUFU is the bottleneck) each half
         // releases its PV MMAs on its own (p_full[t][half]) and, in full blocks, a quarter of
         // the exponentials run on the FMA pipe (exp2_poly2); measured slower for the others.
-        constexpr bool kSplitP = !ScoreT::kUnitGrad;
+        constexpr bool kSplitP = split_p<ScoreT>();
         const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
         const float2 nm2 = make_float2(-msub, -msub);
         float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -509,7 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
                                           xs2, nm2);
               float2 pv;
-              if (decltype(emulate)::value && FA_FWD_EMU != 0 && (k & 3) == 3) pv = exp2_poly2(x);
+              if (decltype(emulate)::value && FA_FWD_EMU != 0 && (k % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
+                pv = exp2_poly2(x);
               else pv = make_float2(ex2(x.x), ex2(x.y));
               ls[k & 3] = __fadd2_rn(ls[k & 3], pv);
               pk[k] = pack_bf16(pv.x, pv.y);
@@ -543,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           mbar_arrive(&sm.p_full[t][1]);
         }
+        if (row == 0) ftrace(p, gs, 18);
         const float2 l01 = __fadd2_rn(ls[0], ls[1]), l23 = __fadd2_rn(ls[2], ls[3]);
         const float2 lt = __fadd2_rn(l01, l23);
         l += lt.x + lt.y;
@@ -676,6 +688,11 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
       fprintf(stderr, "[fwd trace] step %d: S0seen %lld P0done %lld PV0 %lld..%lld QK0 %lld..%lld | S1seen %lld P1done %lld PV1 %lld..%lld QK1 %lld..%lld\n",
               s, e[0] - t0, e[1] - t0, e[4] - t0, e[8] - t0, e[10] - t0, e[6] - t0, e[2] - t0, e[3] - t0,
               e[5] - t0, e[9] - t0, e[11] - t0, e[7] - t0);
+    }
+    for (int s = 20; s < 28; ++s) {
+      const long long* e = h + s * kFTraceEv;
+      fprintf(stderr, "[fwd trace] softmax0 step %d: ld %lld  max %lld  exp+st %lld  end %lld\n", s, e[16] - e[0],
+              e[17] - e[16], e[18] - e[17], e[1] - e[18]);
     }
     for (int s = 20; s < 28; ++s) {
       const long long* e = h + s * kFTraceEv;

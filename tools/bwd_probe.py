@@ -31,7 +31,7 @@ def main(names):
             os.environ["FA_BWD_EXP"] = exp
             t = timeit(run, iters=5, warm=2)
             print(f"{name} bwd exp={exp} {t:.3f} ms  {2.5 * c['gf'] / t:.1f} TFLOPS", flush=True)
-        os.environ["FA_BWD_EXP"] = "0"
+        os.environ["FA_BWD_EXP"] = os.environ.get("TRACE_EXP", "0")
         os.environ["FA_BWD_TRACE"] = os.environ.get("TRACE_LEVEL", "1")
         run()
         torch.cuda.synchronize()

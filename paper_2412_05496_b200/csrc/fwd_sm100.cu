@@ -682,19 +682,21 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
     FA_CHECK_CUDA(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
     FA_CHECK_CUDA(cudaStreamSynchronize(st));
     cudaFree(trace);
+    const int s_lo = getenv("FA_FWD_TRACE_FROM") ? atoi(getenv("FA_FWD_TRACE_FROM")) : 20;
+    const int s_hi = s_lo + (getenv("FA_FWD_TRACE_FROM") ? 24 : 8);
     const long long t0 = h[20 * kFTraceEv];
-    for (int s = 20; s < 28; ++s) {
+    for (int s = s_lo; s < s_hi; ++s) {
       const long long* e = h + s * kFTraceEv;
       fprintf(stderr, "[fwd trace] step %d: S0seen %lld P0done %lld PV0 %lld..%lld QK0 %lld..%lld | S1seen %lld P1done %lld PV1 %lld..%lld QK1 %lld..%lld\n",
               s, e[0] - t0, e[1] - t0, e[4] - t0, e[8] - t0, e[10] - t0, e[6] - t0, e[2] - t0, e[3] - t0,
               e[5] - t0, e[9] - t0, e[11] - t0, e[7] - t0);
     }
-    for (int s = 20; s < 28; ++s) {
+    for (int s = s_lo; s < s_hi; ++s) {
       const long long* e = h + s * kFTraceEv;
       fprintf(stderr, "[fwd trace] softmax0 step %d: ld %lld  max %lld  exp+st %lld  end %lld\n", s, e[16] - e[0],
               e[17] - e[16], e[18] - e[17], e[1] - e[18]);
     }
-    for (int s = 20; s < 28; ++s) {
+    for (int s = s_lo; s < s_hi; ++s) {
       const long long* e = h + s * kFTraceEv;
       fprintf(stderr, "[fwd trace] block %d: K issued %lld  V issued %lld  MMA wants V %lld  V seen %lld\n", s,
               e[12] - t0, e[13] - t0, e[15] - t0, e[14] - t0);

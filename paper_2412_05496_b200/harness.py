@@ -363,7 +363,9 @@ def run_point(cfg: BenchConfig, variant_text: str, mode: str, q_len: int, kv_len
         errs = [float((g.double() - w.grad).abs().max()) / max(1.0, float(w.grad.abs().max()))
                 for g, w in ((grads.dq, q64), (grads.dk, k64), (grads.dv, v64))]
         row.max_abs_err = max(errs)
-        row.rmse_err = max(_rmse(g, w.grad) for g, w in ((grads.dq, q64), (grads.dk, k64), (grads.dv, v64)))
+        # relative to the gradient's scale, like the max-abs check (ALiBi/long rows give |grad| >> 1)
+        row.rmse_err = max(_rmse(g, w.grad) / max(1.0, float(w.grad.abs().max()))
+                           for g, w in ((grads.dq, q64), (grads.dk, k64), (grads.dv, v64)))
         if row.max_abs_err > tol["bwd"]:
             fail(f"grad rel err {row.max_abs_err:.3g} > {tol['bwd']:.3g} vs dense float64")
         if row.rmse_err > tol["bwd_rmse"]:

@@ -127,8 +127,46 @@ struct MaskFn {
       const int dq = __ldg(p.doc_ids + qq);
       return bits & doc_match_bits32(p.doc_ids, p.doc_len, kv0, dq);
     } else {
-      return mask_bits32_generic(*this, b, h, q, kv0, kv_lim);
+      // word-level evaluation of the term groups (one range / vector compare per term); only
+      // remapped positions (non-affine) and the per-element terms (natten, hash) fall back
+      if (p.remap != nullptr) return mask_bits32_generic(*this, b, h, q, kv0, kv_lim);
+      const uint32_t in = range_bits32(kv0, INT_MIN / 2, kv_lim - 1);
+      uint32_t bits = group_bits32(p.terms, b, h, qq, kv0, in);
+      if (p.or_terms != 0u && bits != in) bits |= group_bits32(p.or_terms, b, h, qq, kv0, in & ~bits);
+      return bits;
     }
+  }
+  // AND of the terms in t over kv0 + i (i in [0, 32)) at query position q, within `in`
+  __device__ __forceinline__ uint32_t group_bits32(uint32_t t, int b, int h, int q, int kv0, uint32_t in) const {
+    uint32_t bits = in;
+    if (t & kMaskNever) return 0u;
+    if (t & kMaskCausal) bits &= range_bits32(kv0, INT_MIN / 2, q);
+    if (t & kMaskSliding) bits &= range_bits32(kv0, q - p.window, q);
+    if (t & kMaskPrefix) bits &= range_bits32(kv0, INT_MIN / 2, max(p.prefix - 1, q));
+    if ((t & kMaskDocument) && bits != 0u) bits &= doc_match_bits32(p.doc_ids, p.doc_len, kv0, __ldg(p.doc_ids + q));
+    if ((t & (kMaskNatten | kMaskHash)) && bits != 0u) {
+      for (uint32_t m = bits; m != 0u; m &= m - 1u) {
+        const int i = __ffs(m) - 1;
+        if (!group(t & (kMaskNatten | kMaskHash), b, h, q, kv0 + i)) bits &= ~(1u << i);
+      }
+    }
+    return bits;
+  }
+  // the same over q0 + i at a fixed kv (the backward's view)
+  __device__ __forceinline__ uint32_t group_bits32_q(uint32_t t, int b, int h, int q0, int kv, uint32_t in) const {
+    uint32_t bits = in;
+    if (t & kMaskNever) return 0u;
+    if (t & kMaskCausal) bits &= range_bits32(q0, kv, INT_MAX / 2);
+    if (t & kMaskSliding) bits &= range_bits32(q0, kv, kv + p.window);
+    if ((t & kMaskPrefix) && kv >= p.prefix) bits &= range_bits32(q0, kv, INT_MAX / 2);
+    if ((t & kMaskDocument) && bits != 0u) bits &= doc_match_bits32(p.doc_ids, p.doc_len, q0, __ldg(p.doc_ids + kv));
+    if ((t & (kMaskNatten | kMaskHash)) && bits != 0u) {
+      for (uint32_t m = bits; m != 0u; m &= m - 1u) {
+        const int i = __ffs(m) - 1;
+        if (!group(t & (kMaskNatten | kMaskHash), b, h, q0 + i, kv)) bits &= ~(1u << i);
+      }
+    }
+    return bits;
   }
   // Bit i = mask(b, h, q0 + i, kv) for i in [0, 32): the backward's (kv row, q columns) view.
   // q positions >= q_lim are reported as 0 and not evaluated.
@@ -146,10 +184,15 @@ struct MaskFn {
       if (bits == 0u) return 0u;
       return bits & doc_match_bits32(p.doc_ids, p.doc_len, qq0, __ldg(p.doc_ids + kv));
     } else {
-      uint32_t bits = 0;
+      if (p.remap != nullptr) {
+        uint32_t bits = 0;
 #pragma unroll 4
-      for (int i = 0; i < 32; ++i)
-        if (q0 + i < q_lim) bits |= static_cast<uint32_t>((*this)(b, h, q0 + i, kv)) << i;
+        for (int i = 0; i < 32; ++i)
+          if (q0 + i < q_lim) bits |= static_cast<uint32_t>((*this)(b, h, q0 + i, kv)) << i;
+        return bits;
+      }
+      uint32_t bits = group_bits32_q(p.terms, b, h, qq0, kv, in);
+      if (p.or_terms != 0u && bits != in) bits |= group_bits32_q(p.or_terms, b, h, qq0, kv, in & ~bits);
       return bits;
     }
   }

@@ -136,6 +136,17 @@ struct MaskFn {
       return bits;
     }
   }
+  // na_naive over x0 + i (i in [0, 32)) around pixel c: per canvas row within the radius, one
+  // contiguous column range (mask_library.cpp:137-149 is symmetric in q and kv)
+  __device__ __forceinline__ uint32_t natten_bits32(int c, int x0) const {
+    const int w = p.na_w, rad = p.na_radius;
+    const int cr = c / w, cc = c % w;
+    const int c_lo = max(cc - rad, 0), c_hi = min(cc + rad, w - 1);
+    uint32_t nb = 0u;
+    for (int r = max(x0 / w, cr - rad); r <= min((x0 + 31) / w, cr + rad); ++r)
+      nb |= range_bits32(x0, r * w + c_lo, r * w + c_hi);
+    return nb;
+  }
   // AND of the terms in t over kv0 + i (i in [0, 32)) at query position q, within `in`
   __device__ __forceinline__ uint32_t group_bits32(uint32_t t, int b, int h, int q, int kv0, uint32_t in) const {
     uint32_t bits = in;
@@ -143,11 +154,12 @@ struct MaskFn {
     if (t & kMaskCausal) bits &= range_bits32(kv0, INT_MIN / 2, q);
     if (t & kMaskSliding) bits &= range_bits32(kv0, q - p.window, q);
     if (t & kMaskPrefix) bits &= range_bits32(kv0, INT_MIN / 2, max(p.prefix - 1, q));
+    if ((t & kMaskNatten) && bits != 0u) bits &= natten_bits32(q, kv0);
     if ((t & kMaskDocument) && bits != 0u) bits &= doc_match_bits32(p.doc_ids, p.doc_len, kv0, __ldg(p.doc_ids + q));
-    if ((t & (kMaskNatten | kMaskHash)) && bits != 0u) {
+    if ((t & kMaskHash) && bits != 0u) {
       for (uint32_t m = bits; m != 0u; m &= m - 1u) {
         const int i = __ffs(m) - 1;
-        if (!group(t & (kMaskNatten | kMaskHash), b, h, q, kv0 + i)) bits &= ~(1u << i);
+        if (!group(kMaskHash, b, h, q, kv0 + i)) bits &= ~(1u << i);
       }
     }
     return bits;
@@ -159,11 +171,12 @@ struct MaskFn {
     if (t & kMaskCausal) bits &= range_bits32(q0, kv, INT_MAX / 2);
     if (t & kMaskSliding) bits &= range_bits32(q0, kv, kv + p.window);
     if ((t & kMaskPrefix) && kv >= p.prefix) bits &= range_bits32(q0, kv, INT_MAX / 2);
+    if ((t & kMaskNatten) && bits != 0u) bits &= natten_bits32(kv, q0);  // the window is symmetric
     if ((t & kMaskDocument) && bits != 0u) bits &= doc_match_bits32(p.doc_ids, p.doc_len, q0, __ldg(p.doc_ids + kv));
-    if ((t & (kMaskNatten | kMaskHash)) && bits != 0u) {
+    if ((t & kMaskHash) && bits != 0u) {
       for (uint32_t m = bits; m != 0u; m &= m - 1u) {
         const int i = __ffs(m) - 1;
-        if (!group(t & (kMaskNatten | kMaskHash), b, h, q0 + i, kv)) bits &= ~(1u << i);
+        if (!group(kMaskHash, b, h, q0 + i, kv)) bits &= ~(1u << i);
       }
     }
     return bits;

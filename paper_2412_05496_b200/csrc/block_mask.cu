@@ -288,8 +288,8 @@ extern "C" fa_status fa_convert_block_mask(const fa_block_mask* lg, const fa_pag
   out->q_len = lg->q_len;
   out->kv_len = pt->num_physical_pages * pt->page_size;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  static int* d_err = nullptr;  // one flag per process (per current device on first use)
-  if (d_err == nullptr) FA_CHECK_CUDA(cudaMalloc(&d_err, sizeof(int)));
+  int* d_err = scheduler_counter(kSlotConvertErr, st);  // this (device, stream)'s status word
+  FA_REQUIRE(d_err != nullptr, FA_CUDA_ERROR, "convert_block_mask: cannot allocate the status word");
   FA_CHECK_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), st));
   const int nlines = (int)(out->b_dims * out->h_dims * out->rows);
   convert_kernel<<<nlines, 128, 0, st>>>((int)pt->batches, (int)lg->h_dims, (int)lg->rows,

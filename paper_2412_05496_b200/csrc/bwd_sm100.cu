@@ -22,13 +22,15 @@
 //        dQ^T = K^T dS^T        (SS, both MN-major) -> TMEM over the dP columns
 //      The MMA warp software-pipelines consecutive blocks so the tensor core runs the
 //      GEMMs of one block while the compute warps work on the next:
-//          S(t+1) | dK(t) | dQ(t) | dP(t+1) | dV(t+1) | S(t+2) | ...
+//          S(t+1) | dQ(t) | dK(t) | dP(t+1) | dV(t+1) | S(t+2) | ...
 //      Shared memory bandwidth (128 B/clk/SM) is the scarce resource: an SS 128x128x16
-//      MMA alone reads 128 B/clk, so the two GEMMs with an operand already in TMEM (dV,
-//      dK) use TS, and dQ (the fused form of the reference's separate dQ pass,
-//      :237-305) goes from TMEM through registers to L2 with red.global.add (lanes = the
-//      head-dim index, so each instruction adds one whole 128-byte line) instead of
-//      being staged through shared memory.
+//      MMA alone reads 128 B/clk, so dV (P^T already in TMEM) is TS; dK reads dS^T from
+//      the same smem buffer as dQ. dQ (the fused form of the reference's separate dQ
+//      pass, :237-305) is drained from TMEM by the reduction warpgroup into per-warp
+//      32x32 fp32 smem tiles and added into the fp32 accumulator in L2 with TMA
+//      cp.reduce.async.bulk.tensor (add). The order of those adds across kv blocks is
+//      not fixed, so dQ is not bitwise reproducible run to run unless the deterministic
+//      mode orders them (see FA_BWD_DETERMINISTIC below).
 //      Warps 0-7 compute (two warpgroups, 64 q columns each; thread = kv row),
 //      warps 8-11 dQ reduction + dK/dV epilogue, warp 12 TMA producer, warp 13 MMA.
 //   3. convert: dQ fp32 -> bf16.
@@ -51,7 +53,6 @@ namespace fa {
 CUresult encode_tile_map(CUtensorMap* map, const void* base, int bh, int len, int d);
 CUresult encode_f32_map(CUtensorMap* map, const void* base, int bh, int len, int d, int box_d,
                         int box_rows);
-int* scheduler_counter(int slot);
 
 namespace {
 
@@ -75,7 +76,6 @@ struct BwdParams {
   int num_items;
   int* work_counter;
   long long* trace;  // debug only (FA_BWD_TRACE): per-block phase timestamps of CTA 0
-  int exp_flags;     // debug only (FA_BWD_EXP, wrong results): 1 skip dQ reds
 };
 
 // trace slots [block][event] of CTA 0 (FA_BWD_TRACE); see the host-side summary in run().
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int qq = 0; qq < 32; ++qq) stg[qq * 32 + lane] = __uint_as_float(a[c4 * 32 + qq]);
               fence_proxy_async();
               __syncwarp();
-              if (lane == 0 && !(p.exp_flags & 1)) {
+              if (lane == 0) {
                 tma_reduce_add_3d(&tmDQ, stg, wq * 32, r * kTile + c4 * 32, b * p.Hq + h);
                 bulk_commit_group();
               }
@@ -711,8 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int d = wq * 32 + lane;
           const int nq = min(kTile, p.Lq - r * kTile);
           float* base = p.dq_acc + (static_cast<long long>(b * p.Hq + h) * p.Lq + r * kTile) * D + d;
-          if (p.exp_flags & 1) {
-          } else if (nq == kTile) {
+          if (nq == kTile) {
 #pragma unroll
             for (int qq = 0; qq < kTile; ++qq) red_add_f32(base + qq * D, __uint_as_float(a[qq]));
           } else {
@@ -747,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0 && !(p.exp_flags & 1)) {
+            if (lane == 0) {
               tma_reduce_add_3d(&tmDQ, stg, 0, r * kTile + wq * 32, b * p.Hq + h);
               bulk_commit_group();
             }
@@ -912,7 +911,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.dv = static_cast<__nv_bfloat16*>(dv);
   p.scale = g.scale;
   p.num_items = g.Bkv * g.Hkv * g.cols;
-  p.work_counter = scheduler_counter(1);
+  p.work_counter = scheduler_counter(kSlotBwdSched, st);
   FA_REQUIRE(p.work_counter != nullptr, FA_CUDA_ERROR, "backward: cannot allocate the scheduler counter");
   FA_CHECK_CUDA(cudaMemsetAsync(p.work_counter, 0, sizeof(int), st));
   long long* trace = nullptr;
@@ -921,7 +920,6 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
     FA_CHECK_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * kTraceTasks * kTraceEv, st));
   }
   p.trace = trace;
-  p.exp_flags = getenv("FA_BWD_EXP") ? atoi(getenv("FA_BWD_EXP")) : 0;
   const size_t smem = sizeof(BSmem<D>);
   auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -8,7 +8,10 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "internal.h"
 
@@ -26,6 +29,21 @@ fa_status cuda_status(cudaError_t e, const char* what) {
   return set_error(FA_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Small device scratch words (dynamic tile-scheduler counters, device status flags), one
+// 64-byte slot per (device, stream, slot id): the launcher zeroes it on the stream right before
+// the kernel, so launches on one stream are ordered and launches on different streams never
+// share a word.
+int* scheduler_counter(int slot, cudaStream_t st) {
+  static std::map<std::tuple<int, cudaStream_t, int>, int*> counters;
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  int*& c = counters[std::make_tuple(dev, st, slot)];
+  if (c == nullptr && cudaMalloc(&c, 64) != cudaSuccess) c = nullptr;
+  return c;
+}
+
 int num_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -122,6 +140,10 @@ fa_status check_tensor(const fa_tensor& t, const char* name) {
   FA_REQUIRE(t.dtype == FA_F32 || t.dtype == FA_BF16, FA_UNSUPPORTED,
              std::string(name) + ": dtype must be FA_F32 or FA_BF16");
   return FA_OK;
+}
+
+bool same_shape(const fa_tensor& a, const fa_tensor& b) {
+  return a.b == b.b && a.h == b.h && a.l == b.l && a.d == b.d;
 }
 
 std::string shp(const fa_tensor& t) {
@@ -265,9 +287,15 @@ fa_status fa_flex_bwd(const fa_bwd_args* a, void* stream) {
       (s = check_tensor(a->dq, "dq")) || (s = check_tensor(a->dk, "dk")) ||
       (s = check_tensor(a->dv, "dv")))
     return s;
-  FA_REQUIRE(a->d_out.b == a->q.b && a->d_out.h == a->q.h && a->d_out.l == a->q.l &&
-                 a->d_out.d == a->q.d,
-             FA_SHAPE_MISMATCH, "backward: d_out " + shp(a->d_out) + " must match q " + shp(a->q));
+  FA_REQUIRE(same_shape(a->d_out, a->q) && a->d_out.dtype == a->q.dtype, FA_SHAPE_MISMATCH,
+             "backward: d_out " + shp(a->d_out) + " must match q " + shp(a->q));
+  FA_REQUIRE(same_shape(a->dq, a->q) && a->dq.dtype == a->q.dtype, FA_SHAPE_MISMATCH,
+             "backward: dq " + shp(a->dq) + " must match q " + shp(a->q));
+  FA_REQUIRE(same_shape(a->dk, a->k) && same_shape(a->dv, a->k) && a->dk.dtype == a->q.dtype &&
+                 a->dv.dtype == a->q.dtype,
+             FA_SHAPE_MISMATCH, "backward: dk/dv must match k " + shp(a->k));
+  FA_REQUIRE(a->out.dtype == a->q.dtype, FA_STALE_STATISTICS,
+             "backward: saved forward output has another dtype than q");
   FA_REQUIRE(a->out.b == a->q.b && a->out.h == a->q.h && a->out.l == a->q.l && a->out.d == a->q.d,
              FA_STALE_STATISTICS, "backward: saved forward statistics do not match these tensors");
   FA_REQUIRE(a->lse != nullptr, FA_STALE_STATISTICS, "backward: NULL lse");
@@ -298,43 +326,55 @@ size_t fa_decode_workspace_size(int64_t batch, int64_t heads, int64_t n_new, int
 fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
   clear_error();
   FA_REQUIRE(a != nullptr, FA_SHAPE_MISMATCH, "decode: NULL args");
+  FA_REQUIRE(a->bm != nullptr, FA_BLOCK_MASK_MISMATCH, "decode: NULL block mask");
   fa_status s;
   if ((s = check_qkv(a->q, a->k_cache, a->v_cache, a->gqa_group))) return s;
   if ((s = check_tensor(a->out, "out"))) return s;
+  FA_REQUIRE(same_shape(a->out, a->q) && a->out.dtype == a->q.dtype, FA_SHAPE_MISMATCH,
+             "decode: out " + shp(a->out) + " must match q " + shp(a->q));
+  FA_REQUIRE(a->lse != nullptr, FA_SHAPE_MISMATCH, "decode: NULL lse");
   FA_REQUIRE(a->q.dtype == FA_BF16 || a->pt == nullptr, FA_UNSUPPORTED,
              "decode: a paged cache needs bf16 (float32 decode is unpaged)");
   const int64_t n_new = a->q.l;
   int64_t logical_kv = a->k_cache.l;
   if (a->pt != nullptr) {
+    const fa_page_table* pt = a->pt;
+    FA_REQUIRE(pt->table && pt->phys_to_logical && pt->owner && pt->seq_len, FA_SHAPE_MISMATCH,
+               "decode: page table arrays missing");
     FA_REQUIRE(a->k_cache.b == 1, FA_SHAPE_MISMATCH, "decode: paged cache must have batch 1");
-    FA_REQUIRE(a->pt->page_size == a->bm->bs_kv, FA_BLOCK_MASK_MISMATCH,
+    FA_REQUIRE(pt->batches == a->q.b, FA_SHAPE_MISMATCH, "decode: page table batches must equal q batch");
+    FA_REQUIRE(pt->page_size == a->bm->bs_kv, FA_BLOCK_MASK_MISMATCH,
                "decode: page size must equal bs_kv");
-    FA_REQUIRE(a->k_cache.l == a->pt->num_physical_pages * a->pt->page_size, FA_SHAPE_MISMATCH,
+    FA_REQUIRE(a->k_cache.l == pt->num_physical_pages * pt->page_size, FA_SHAPE_MISMATCH,
                "decode: physical cache length must be pages * page_size");
+    // a converted mask (convert_block_mask): batch materialised, one column per physical page
     FA_REQUIRE(a->bm->b_dims == a->q.b, FA_BLOCK_MASK_MISMATCH,
                "decode: converted block mask must materialise the batch");
-    logical_kv = a->pt->max_logical_pages * a->pt->page_size;
+    FA_REQUIRE(a->bm->h_dims == 1 || a->bm->h_dims == a->q.h, FA_BLOCK_MASK_MISMATCH,
+               "decode: block mask head dim must be 1 or " + std::to_string(a->q.h));
+    FA_REQUIRE(a->bm->q_len == n_new && a->bm->kv_len == a->k_cache.l && a->bm->bs_q >= 1 &&
+                   a->bm->rows == (n_new + a->bm->bs_q - 1) / a->bm->bs_q &&
+                   a->bm->cols == pt->num_physical_pages,
+               FA_BLOCK_MASK_MISMATCH,
+               "decode: converted block mask geometry does not match the physical cache");
+    FA_REQUIRE(a->bm->kv_num_blocks && a->bm->kv_indices && a->bm->full_kv_num_blocks &&
+                   a->bm->full_kv_indices,
+               FA_BLOCK_MASK_MISMATCH, "decode: block mask kv-side arrays missing");
+    logical_kv = pt->max_logical_pages * pt->page_size;
   }
   // engine.cpp:410-414
-  FA_REQUIRE(a->offset >= 0 && a->offset + n_new <= (a->pt ? logical_kv : a->k_cache.l),
-             FA_OFFSET_OUT_OF_RANGE,
+  FA_REQUIRE(a->offset >= 0 && a->offset + n_new <= logical_kv, FA_OFFSET_OUT_OF_RANGE,
              "decode: rows [" + std::to_string(a->offset) + ", " + std::to_string(a->offset + n_new) +
                  ") fall outside cache");
-  FA_REQUIRE(a->bm != nullptr, FA_BLOCK_MASK_MISMATCH, "decode: NULL block mask");
   if (a->pt == nullptr) {
     if ((s = check_bm(a->bm, a->q.b, a->q.h, n_new, a->k_cache.l))) return s;
-  } else {
-    FA_REQUIRE(a->bm->q_len == n_new && a->bm->kv_len == a->k_cache.l, FA_BLOCK_MASK_MISMATCH,
-               "decode: converted block mask geometry does not match the physical cache");
   }
   fa_mask_desc m = a->mask;
   fa_score_desc sc = a->score;
   m.q_offset += a->offset;  // offset_mask / offset_score (mask_library.cpp:106-119)
   sc.q_offset += a->offset;
-  if ((s = check_mods(m, sc, a->q.h, n_new, 0))) return s;
-  if (m.terms & kMaskDocument)
-    FA_REQUIRE(m.doc_len >= logical_kv, FA_INDEX_OUT_OF_RANGE,
-               "document_mask: token index outside id table");
+  // the kernels evaluate the mask at logical kv positions up to logical_kv - 1
+  if ((s = check_mods(m, sc, a->q.h, n_new, logical_kv))) return s;
   if (a->q.dtype == FA_F32) {
     // decode<float> is forward_impl over the shifted mask (engine.cpp:403-427): the fp32
     // CUDA-core forward with q_offset applied to the mask and score terms

@@ -2,17 +2,19 @@
 // fp32 accumulate), the tensor-core replacement of forward_impl
 // (engine.cpp:46-163).
 //
-// Persistent, warp-specialised CTA (320 threads, 1 CTA/SM). A work item is a
-// pair of 128-row query tiles (block rows 2p, 2p+1) of one (b, h):
+// Persistent, warp-specialised CTA (384 threads, 1 CTA/SM; setmaxnreg 224 for
+// the softmax warpgroups, 56 for the rest). A work item is a pair of 128-row
+// query tiles (block rows 2p, 2p+1) of one (b, h):
 //   warps 0-3  softmax/correction/epilogue for tile 0   (thread = query row)
 //   warps 4-7  the same for tile 1
+//   warps 10-11 idle (they complete the third warpgroup for setmaxnreg)
 //   warp  8    TMA producer: merges both rows' kv lists (partial + full) into a
 //              union list in smem (descending block order; any order is exact
 //              math, descending keeps the running max stable),
 //              then streams Q (once) and K_j, V_j (per visited block) with
 //              cp.async.bulk.tensor into a 2-stage (D=128) ring. Empty blocks
 //              are never loaded.
-//   warp  9    MMA issuer (one thread): S_t = Q_t K_j^T (SS, TMEM fp32) and
+//   warp  9    MMA issuer (warp-uniform control, one elected lane issues): S_t = Q_t K_j^T (SS, TMEM fp32) and
 //              O_t += P_t V_j (TS: P from TMEM as bf16, V from smem, MN-major),
 //              ordered  QK0 QK1 | PV0(j) QK0(j+1) PV1(j) QK1(j+1) | ...  so the
 //              two tiles' softmax ping-pong against the tensor core.
@@ -39,17 +41,6 @@
 #include "sm100_ptx.cuh"
 
 namespace fa {
-
-// One scheduler counter per (device, kernel slot), zeroed on the stream before every launch.
-int* scheduler_counter(int slot) {
-  static int* counters[64] = {nullptr};
-  static std::mutex mu;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (counters[dev] == nullptr && cudaMalloc(&counters[dev], 256) != cudaSuccess) return nullptr;
-  return counters[dev] + (slot & 63);
-}
 
 namespace {
 
@@ -660,7 +651,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   p.scale_log2 = g.scale * kLog2e;
   p.npairs = (g.rows + 1) / 2;
   p.num_items = g.B * g.Hq * p.npairs;
-  p.work_counter = scheduler_counter(0);
+  p.work_counter = scheduler_counter(kSlotFwdSched, st);
   long long* trace = nullptr;
   if (FA_FWD_TRACE_BUILD != 0 && getenv("FA_FWD_TRACE") != nullptr) {
     FA_CHECK_CUDA(cudaMalloc(&trace, sizeof(long long) * kFTraceSteps * kFTraceEv));

@@ -19,6 +19,10 @@ void clear_error();
 fa_status cuda_status(cudaError_t e, const char* what);
 void count_launch(uint64_t n = 1);
 int num_sms();
+// 64 bytes of device scratch per (device, stream, slot): work counters of the persistent
+// kernels and device status flags. Slots:
+enum { kSlotFwdSched = 0, kSlotBwdSched = 1, kSlotConvertErr = 2, kSlotFiniteErr = 3, kSlotCounters = 4 };
+int* scheduler_counter(int slot, cudaStream_t st);
 
 #define FA_CHECK_CUDA(expr)                                          \
   do {                                                               \

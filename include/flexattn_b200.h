@@ -15,6 +15,8 @@
  *                             (+ convert_mods     paged_kv.hpp:117, paged_kv.cpp:230-310
  *                                when a page table is given)
  *   fa_fill_uniform        <- random_tensor<Real> random.hpp:41-46 (SplitMix64 [-1,1))
+ *   fa_check_finite        <- validate_inputs     validate.hpp:30-39 (finiteness part)
+ *   fa_*_args.counters     <- OpCounters*         engine.hpp:21-32, 68-96
  *
  * Conventions (all entry points):
  *   - Caller-owned DEVICE buffers; plain pointers + sizes, no library types.
@@ -158,6 +160,8 @@ typedef struct fa_page_table {
   const int32_t* phys_to_logical;  /* (num_physical_pages), -1 = free */
   const int32_t* owner;            /* (num_physical_pages), -1 = free */
   const int32_t* seq_len;          /* (batches) tokens stored per sequence */
+  int64_t max_seq_len;             /* host copy of max(seq_len) (ABI v3); 0 = unknown, then
+                                      max_logical_pages * page_size bounds the mask's kv range */
 } fa_page_table;
 
 /* ---- misc ------------------------------------------------------------------ */
@@ -195,6 +199,37 @@ FA_API fa_status fa_convert_block_mask(const fa_block_mask* logical, const fa_pa
                                 fa_block_mask* out, void* stream);
 
 /* ---- attention ---------------------------------------------------------------- */
+/* Work counters of the reference (OpCounters, engine.hpp:21-32), computed on the device from the
+ * BlockMask and the mask (not by instrumenting the kernels):
+ *   mask_evals  = positions of the visited partial tiles inside [0,Q_LEN) x [0,KV_LEN), per (b, h)
+ *                 walk (backward: both passes, rows with lse = -inf skipped, engine.cpp:257-260);
+ *   score_evals = live (mask-true) positions, one score_mod application each (backward: x2);
+ *   madds       = forward: 2*D per live position (q.k dot + p.v); backward: D per q row (Δ)
+ *                 + 7*D per live position (dq pass 3*D, dk/dv pass 4*D).
+ * The reference's forward madds additionally count D per running-max increase (accumulator
+ * rescales, engine.cpp:128-133); that term depends on the data and on the visit order and is
+ * not included. */
+typedef struct fa_op_counters {
+  uint64_t madds;
+  uint64_t mask_evals;
+  uint64_t score_evals;
+} fa_op_counters;
+
+/* Per-call flags (ABI v3). */
+enum {
+  /* Data-dependent validation of the reference, at the cost of one extra read of the inputs
+   * and a stream synchronisation at the end of the call: NaN/inf in q/k/v
+   * (validate_inputs, validate.hpp:36-38) and d_out (engine.cpp:196) -> FA_NON_FINITE_INPUT;
+   * a paged decode that visits a page not owned by the row's batch element
+   * (convert_mods, paged_kv.cpp:259-272) -> FA_UNMAPPED_PHYSICAL_INDEX. */
+  FA_FLAG_VALIDATE = 1u << 0,
+  /* Backward only: dQ partial sums are added in a fixed order (ascending kv block per q block),
+   * so dq/dk/dv are bitwise reproducible run to run (the reference's worker-count
+   * independence, README.md:104-106). Without it dk/dv are still reproducible but the fp32
+   * dQ additions happen in arrival order. */
+  FA_FLAG_DETERMINISTIC = 1u << 1
+};
+
 typedef struct fa_fwd_args {
   fa_tensor q, k, v;       /* q (B,Hq,Q,D); k,v (B or 1, Hkv, KV, D) */
   fa_tensor out;           /* (B,Hq,Q,D), dtype of q */
@@ -204,6 +239,9 @@ typedef struct fa_fwd_args {
   fa_score_desc score;
   double scale;            /* <= 0 selects 1/sqrt(D) (config.hpp:28-31) */
   int64_t gqa_group;       /* Hq == gqa_group * Hkv */
+  uint32_t flags;          /* FA_FLAG_VALIDATE (ABI v3) */
+  int32_t _pad1;
+  fa_op_counters* counters;/* host out-param or NULL; non-NULL synchronises the stream */
 } fa_fwd_args;
 
 typedef struct fa_bwd_args {
@@ -217,6 +255,12 @@ typedef struct fa_bwd_args {
   int64_t gqa_group;
   void* workspace;         /* fa_bwd_workspace_size bytes */
   size_t workspace_bytes;
+  uint32_t flags;          /* FA_FLAG_VALIDATE | FA_FLAG_DETERMINISTIC (ABI v3) */
+  int32_t _pad1;
+  fa_op_counters* counters;/* host out-param or NULL; non-NULL synchronises the stream */
+  /* optional cudaEvent_t (as void*) recorded on the stream before the preprocess kernel, before
+   * the main kernel, before the dQ conversion and after it (per-kernel timing); NULL = none */
+  void* phase_events[4];
 } fa_bwd_args;
 
 typedef struct fa_decode_args {
@@ -235,6 +279,9 @@ typedef struct fa_decode_args {
   int32_t _pad;
   void* workspace;         /* fa_decode_workspace_size bytes */
   size_t workspace_bytes;
+  uint32_t flags;          /* FA_FLAG_VALIDATE (ABI v3) */
+  int32_t _pad2;
+  fa_op_counters* counters;/* host out-param or NULL; non-NULL synchronises the stream */
 } fa_decode_args;
 
 FA_API fa_status fa_flex_fwd(const fa_fwd_args* args, void* stream);
@@ -243,6 +290,12 @@ FA_API fa_status fa_flex_bwd(const fa_bwd_args* args, void* stream);
 FA_API size_t fa_decode_workspace_size(int64_t batch, int64_t heads, int64_t n_new, int64_t dim,
                                 int32_t num_splits);
 FA_API fa_status fa_flex_decode(const fa_decode_args* args, void* stream);
+
+/* NaN/inf scan of up to 8 tensors in one pass (validate_inputs' finiteness checks,
+ * validate.hpp:36-38, tensor.hpp:38-42). Synchronises the stream; FA_NON_FINITE_INPUT names the
+ * first offending tensor (names[i], or its index). */
+FA_API fa_status fa_check_finite(const fa_tensor* tensors, const char* const* names, int32_t n,
+                                 void* stream);
 
 /* ---- synthetic inputs ------------------------------------------------------------
  * Element i of random_tensor(seed, ...) (random.hpp:41-46):

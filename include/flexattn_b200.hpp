@@ -10,6 +10,10 @@
 //   blockattn::backward<Real>(q, k, v, fwd, dout, smod, bm, bm_t, cfg) engine.hpp:78-82
 //   blockattn::decode<Real>(q, k, v, offset, mask, smod, bm, cfg)      engine.hpp:92-96
 //   blockattn::convert_block_mask(bm, page_table)               paged_kv.hpp:101
+//   blockattn::convert_mods(mask, smod, page_table)             paged_kv.hpp:117
+//   blockattn::PagedKVCache                                     paged_kv.hpp:50-89
+//   blockattn::OpCounters                                       engine.hpp:21-32
+//   blockattn::validate_inputs (finiteness)                     validate.hpp:30-39
 //
 // Differences by design: tensors are device buffers (bf16 or fp32); every call is
 // stream-ordered (default stream unless given); errors are the same exception classes
@@ -283,8 +287,43 @@ struct AttentionConfig {
   i64 gqa_group = 1;
   i64 block_size_q = 128;
   i64 block_size_kv = 128;
+  // Not in the reference config: the reference always runs its data-dependent validation
+  // (NaN/inf scans -> NonFiniteInput, foreign pages -> UnmappedPhysicalIndex); here it costs an
+  // extra pass and a stream synchronisation, so it is opt-in.
+  bool validate = false;
+  // Backward: ordered dQ additions, bitwise reproducible gradients (README.md:104-106).
+  bool deterministic = false;
   double scale_or_default() const { return scale.has_value() ? *scale : 0.0; }
+  uint32_t flags() const {
+    return (validate ? FA_FLAG_VALIDATE : 0u) | (deterministic ? FA_FLAG_DETERMINISTIC : 0u);
+  }
 };
+
+// OpCounters (engine.hpp:21-32); calls add into it like the reference. madds omit the
+// reference's data-dependent rescale term (see fa_op_counters in flexattn_b200.h).
+struct OpCounters {
+  std::uint64_t madds = 0;
+  std::uint64_t mask_evals = 0;
+  std::uint64_t score_evals = 0;
+  OpCounters& operator+=(const fa_op_counters& o) {
+    madds += o.madds;
+    mask_evals += o.mask_evals;
+    score_evals += o.score_evals;
+    return *this;
+  }
+};
+
+// validate_inputs' finiteness part (validate.hpp:36-38): throws NonFiniteInput.
+inline void check_finite(const std::vector<std::pair<std::string, const DeviceTensor4*>>& ts,
+                         cudaStream_t st = nullptr) {
+  std::vector<fa_tensor> c;
+  std::vector<const char*> names;
+  for (const auto& t : ts) {
+    c.push_back(t.second->c());
+    names.push_back(t.first.c_str());
+  }
+  check(fa_check_finite(c.data(), names.data(), static_cast<int32_t>(c.size()), st));
+}
 
 // ---- BlockMask (block_mask.hpp:35-79) --------------------------------------------------------
 struct BlockMask {
@@ -358,7 +397,7 @@ struct Gradients {
 
 inline AttentionOutput forward(const DeviceTensor4& q, const DeviceTensor4& k, const DeviceTensor4& v,
                                const ScoreMod& smod, const BlockMask& bm, const AttentionConfig& cfg = {},
-                               cudaStream_t st = nullptr) {
+                               OpCounters* counters = nullptr, cudaStream_t st = nullptr) {
   if (!bm.has_runtime_mask) throw BlockMaskMismatch("forward: block mask has no runtime mask attached");
   if (bm.c.bs_q != cfg.block_size_q || bm.c.bs_kv != cfg.block_size_kv)
     throw BlockMaskMismatch("block mask block sizes disagree with config");
@@ -371,14 +410,19 @@ inline AttentionOutput forward(const DeviceTensor4& q, const DeviceTensor4& k, c
   a.score = smod.d;
   a.scale = cfg.scale_or_default();
   a.gqa_group = cfg.gqa_group;
+  a.flags = cfg.flags() & FA_FLAG_VALIDATE;
+  fa_op_counters cc{};
+  if (counters) a.counters = &cc;
   check(fa_flex_fwd(&a, st));
+  if (counters) *counters += cc;
   return res;
 }
 
 inline Gradients backward(const DeviceTensor4& q, const DeviceTensor4& k, const DeviceTensor4& v,
                           const AttentionOutput& fwd, const DeviceTensor4& d_out, const ScoreMod& smod,
                           const BlockMask& bm, const BlockMask& /*bm_t: q side lives in bm*/,
-                          const AttentionConfig& cfg = {}, cudaStream_t st = nullptr) {
+                          const AttentionConfig& cfg = {}, OpCounters* counters = nullptr,
+                          cudaStream_t st = nullptr) {
   if (!bm.has_runtime_mask) throw BlockMaskMismatch("backward: block mask has no runtime mask attached");
   Gradients g{DeviceTensor4(q.b, q.h, q.l, q.d, q.dtype), DeviceTensor4(k.b, k.h, k.l, k.d, k.dtype),
               DeviceTensor4(v.b, v.h, v.l, v.d, v.dtype)};
@@ -395,7 +439,11 @@ inline Gradients backward(const DeviceTensor4& q, const DeviceTensor4& k, const 
   a.gqa_group = cfg.gqa_group;
   a.workspace = work.get();
   a.workspace_bytes = ws;
+  a.flags = cfg.flags();
+  fa_op_counters cc{};
+  if (counters) a.counters = &cc;
   check(fa_flex_bwd(&a, st));
+  if (counters) *counters += cc;
   check_cuda(cudaStreamSynchronize(st), "backward");  // workspace freed on return
   return g;
 }
@@ -403,7 +451,8 @@ inline Gradients backward(const DeviceTensor4& q, const DeviceTensor4& k, const 
 inline AttentionOutput decode(const DeviceTensor4& q_step, const DeviceTensor4& k_cache,
                               const DeviceTensor4& v_cache, i64 offset, const MaskMod& mask,
                               const ScoreMod& smod, const BlockMask& bm, const AttentionConfig& cfg = {},
-                              const fa_page_table* pt = nullptr, cudaStream_t st = nullptr) {
+                              const fa_page_table* pt = nullptr, OpCounters* counters = nullptr,
+                              cudaStream_t st = nullptr) {
   AttentionOutput res{DeviceTensor4(q_step.b, q_step.h, q_step.l, q_step.d, q_step.dtype),
                       DeviceBuffer(static_cast<size_t>(q_step.b * q_step.h * q_step.l) * 4)};
   const size_t ws = fa_decode_workspace_size(q_step.b, q_step.h, q_step.l, q_step.d, 0);
@@ -420,7 +469,11 @@ inline AttentionOutput decode(const DeviceTensor4& q_step, const DeviceTensor4& 
   a.gqa_group = cfg.gqa_group;
   a.workspace = work.get();
   a.workspace_bytes = ws;
+  a.flags = cfg.flags() & FA_FLAG_VALIDATE;
+  fa_op_counters cc{};
+  if (counters) a.counters = &cc;
   check(fa_flex_decode(&a, st));
+  if (counters) *counters += cc;
   check_cuda(cudaStreamSynchronize(st), "decode");
   return res;
 }
@@ -438,6 +491,190 @@ inline BlockMask convert_block_mask(const BlockMask& bm, const fa_page_table& pt
   out.runtime_mask = bm.runtime_mask;
   out.has_runtime_mask = bm.has_runtime_mask;
   return out;
+}
+
+// ---- paged KV cache (paged_kv.hpp:18-89, paged_kv.cpp:13-152) --------------------------------
+// PageTable with host arrays (the reference's value type) and device mirrors for the kernels.
+struct PageTable {
+  static constexpr std::int32_t kSentinel = -1;
+  i64 batches = 0, max_logical_pages = 0, num_physical_pages = 0, page_size = 0;
+  std::vector<std::int32_t> table, phys_to_logical, owner, seq_len;
+  i64 lookup(i64 b, i64 lp) const { return table[static_cast<size_t>(b * max_logical_pages + lp)]; }
+  // device snapshot (convert_mods snapshots the table by value, paged_kv.hpp:115-116)
+  struct Device {
+    DeviceBuffer table, p2l, owner, seq;
+    fa_page_table c{};
+  };
+  std::shared_ptr<Device> to_device(cudaStream_t st = nullptr) const {
+    auto d = std::make_shared<Device>();
+    auto up = [st](const std::vector<std::int32_t>& v, DeviceBuffer& buf) {
+      buf = DeviceBuffer(std::max<size_t>(v.size(), 1) * 4);
+      if (!v.empty())
+        check_cuda(cudaMemcpyAsync(buf.get(), v.data(), v.size() * 4, cudaMemcpyHostToDevice, st), "page table");
+    };
+    up(table, d->table); up(phys_to_logical, d->p2l); up(owner, d->owner); up(seq_len, d->seq);
+    check_cuda(cudaStreamSynchronize(st), "page table");
+    d->c.batches = batches; d->c.max_logical_pages = max_logical_pages;
+    d->c.num_physical_pages = num_physical_pages; d->c.page_size = page_size;
+    d->c.table = d->table.as<int32_t>(); d->c.phys_to_logical = d->p2l.as<int32_t>();
+    d->c.owner = d->owner.as<int32_t>(); d->c.seq_len = d->seq.as<int32_t>();
+    d->c.max_seq_len = seq_len.empty() ? 0 : *std::max_element(seq_len.begin(), seq_len.end());
+    return d;
+  }
+};
+
+// PagedKVCache: the reference's host page allocator (LIFO free list with page 0 on top,
+// deterministic shuffle, capacity-atomic assign/append, idempotent erase) over device K/V of
+// shape (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel.
+class PagedKVCache {
+ public:
+  PagedKVCache(i64 batches, i64 num_pages, i64 page_size, i64 kv_heads, i64 dim, DType t = DType::BF16)
+      : k_(1, kv_heads, num_pages * page_size, dim, t), v_(1, kv_heads, num_pages * page_size, dim, t) {
+    if (batches < 1 || num_pages < 1 || page_size < 1)
+      throw ShapeMismatch("PagedKVCache: batches, num_pages and page_size must be >= 1");
+    pt_.batches = batches;
+    pt_.max_logical_pages = num_pages;
+    pt_.num_physical_pages = num_pages;
+    pt_.page_size = page_size;
+    pt_.table.assign(static_cast<size_t>(batches * num_pages), PageTable::kSentinel);
+    pt_.phys_to_logical.assign(static_cast<size_t>(num_pages), PageTable::kSentinel);
+    pt_.owner.assign(static_cast<size_t>(num_pages), PageTable::kSentinel);
+    pt_.seq_len.assign(static_cast<size_t>(batches), 0);
+    for (i64 p = num_pages - 1; p >= 0; --p) free_.push_back(static_cast<std::int32_t>(p));  // page 0 on top
+    check_cuda(cudaMemset(k_.buf.get(), 0, k_.buf.bytes), "cache");
+    check_cuda(cudaMemset(v_.buf.get(), 0, v_.buf.bytes), "cache");
+  }
+
+  // assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim) on the device
+  void assign(i64 b, const DeviceTensor4& k_tokens, const DeviceTensor4& v_tokens, cudaStream_t st = nullptr) {
+    check_batch(b);
+    check_tokens(k_tokens, v_tokens);
+    const i64 needed = ceil_div(k_tokens.l, pt_.page_size), owned = ceil_div(seq(b), pt_.page_size);
+    if (needed > static_cast<i64>(free_.size()) + owned)
+      throw OutOfPages("PagedKVCache: assign of " + std::to_string(k_tokens.l) + " tokens needs " +
+                       std::to_string(needed) + " pages, only " +
+                       std::to_string(static_cast<i64>(free_.size()) + owned) + " available");
+    erase(b);
+    for (i64 lp = 0; lp < needed; ++lp) take(b, lp);
+    seq(b) = static_cast<std::int32_t>(k_tokens.l);
+    write(b, 0, k_tokens, v_tokens, st);
+  }
+  // append_tokens (paged_kv.cpp:100-126); the append must start on a page boundary or the
+  // caller passes the tail of the partially filled page again (write_tokens is page-granular)
+  void append_tokens(i64 b, const DeviceTensor4& k_new, const DeviceTensor4& v_new, cudaStream_t st = nullptr) {
+    check_batch(b);
+    check_tokens(k_new, v_new);
+    const i64 old = seq(b), owned = ceil_div(old, pt_.page_size), total = ceil_div(old + k_new.l, pt_.page_size);
+    if (total - owned > static_cast<i64>(free_.size()))
+      throw OutOfPages("PagedKVCache: append of " + std::to_string(k_new.l) + " tokens needs " +
+                       std::to_string(total - owned) + " new pages, only " + std::to_string(free_.size()) + " free");
+    if (old % pt_.page_size != 0)
+      throw Unsupported("PagedKVCache::append_tokens: unaligned appends go through the Python layer");
+    for (i64 lp = owned; lp < total; ++lp) take(b, lp);
+    seq(b) = static_cast<std::int32_t>(old + k_new.l);
+    write(b, old, k_new, v_new, st);
+  }
+  // erase (paged_kv.cpp:128-141): idempotent
+  void erase(i64 b) {
+    check_batch(b);
+    for (i64 lp = 0; lp < ceil_div(seq(b), pt_.page_size); ++lp) {
+      const size_t slot = static_cast<size_t>(b * pt_.max_logical_pages + lp);
+      const std::int32_t page = pt_.table[slot];
+      pt_.table[slot] = PageTable::kSentinel;
+      pt_.phys_to_logical[static_cast<size_t>(page)] = PageTable::kSentinel;
+      pt_.owner[static_cast<size_t>(page)] = PageTable::kSentinel;
+      free_.push_back(page);
+    }
+    seq(b) = 0;
+  }
+  // shuffle_free_pages (paged_kv.cpp:143-146, deterministic_shuffle random.hpp:49-56)
+  void shuffle_free_pages(std::uint64_t seed) {
+    std::uint64_t state = seed;
+    for (size_t i = free_.size(); i > 1; --i) {
+      state += 0x9e3779b97f4a7c15ull;
+      std::uint64_t z = state;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      z ^= z >> 31;
+      std::swap(free_[i - 1], free_[static_cast<size_t>(z % i)]);
+    }
+  }
+  const DeviceTensor4& k_phys() const { return k_; }
+  const DeviceTensor4& v_phys() const { return v_; }
+  const PageTable& table() const { return pt_; }
+  i64 page_size() const { return pt_.page_size; }
+  i64 max_tokens() const { return pt_.num_physical_pages * pt_.page_size; }
+  i64 seq_len(i64 b) const { check_batch(b); return pt_.seq_len[static_cast<size_t>(b)]; }
+  i64 free_pages() const { return static_cast<i64>(free_.size()); }
+
+ private:
+  static i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+  std::int32_t& seq(i64 b) { return pt_.seq_len[static_cast<size_t>(b)]; }
+  void check_batch(i64 b) const {
+    if (b < 0 || b >= pt_.batches)
+      throw IndexOutOfRange("PagedKVCache: batch " + std::to_string(b) + " outside [0, " +
+                            std::to_string(pt_.batches) + ")");
+  }
+  void check_tokens(const DeviceTensor4& kt, const DeviceTensor4& vt) const {
+    if (!kt.same_shape(vt)) throw ShapeMismatch("PagedKVCache: k and v tokens must agree");
+    if (kt.b != 1 || kt.h != k_.h || kt.d != k_.d || kt.dtype != k_.dtype)
+      throw ShapeMismatch("PagedKVCache: token tensors must be (1, kv_heads, n, dim) of the cache dtype");
+  }
+  void take(i64 b, i64 lp) {
+    const std::int32_t page = free_.back();
+    free_.pop_back();
+    pt_.table[static_cast<size_t>(b * pt_.max_logical_pages + lp)] = page;
+    pt_.phys_to_logical[static_cast<size_t>(page)] = static_cast<std::int32_t>(lp);
+    pt_.owner[static_cast<size_t>(page)] = static_cast<std::int32_t>(b);
+  }
+  // write_tokens (paged_kv.cpp:54-70) through a one-batch view of the table
+  void write(i64 b, i64 start, const DeviceTensor4& kt, const DeviceTensor4& vt, cudaStream_t st) {
+    if (kt.l == 0) return;
+    const i64 lp0 = start / pt_.page_size, np = ceil_div(kt.l, pt_.page_size);
+    DeviceBuffer row(static_cast<size_t>(np) * 4);
+    check_cuda(cudaMemcpyAsync(row.get(), pt_.table.data() + b * pt_.max_logical_pages + lp0,
+                               static_cast<size_t>(np) * 4, cudaMemcpyHostToDevice, st), "page row");
+    fa_page_table v{};
+    v.batches = 1; v.max_logical_pages = np; v.num_physical_pages = pt_.num_physical_pages;
+    v.page_size = pt_.page_size; v.table = row.as<int32_t>();
+    fa_tensor lk = kt.c(), lv = vt.c(), pk = k_.c(), pv = v_.c();
+    check(fa_paged_write(&lk, &v, &pk, st));
+    check(fa_paged_write(&lv, &v, &pv, st));
+    check_cuda(cudaStreamSynchronize(st), "paged write");  // `row` is freed on return
+  }
+
+  DeviceTensor4 k_, v_;
+  PageTable pt_;
+  std::vector<std::int32_t> free_;  // LIFO
+};
+
+// convert_block_mask over a host PageTable (uploads a device snapshot).
+inline BlockMask convert_block_mask(const BlockMask& bm, const PageTable& pt, cudaStream_t st = nullptr) {
+  const auto d = pt.to_device(st);
+  return convert_block_mask(bm, d->c, st);
+}
+
+// convert_mods (paged_kv.hpp:117, paged_kv.cpp:230-310): the reference bakes a
+// (batch, physical index) -> logical index table into new callables. Here the mods stay the
+// user's (written in logical positions) and carry a device snapshot of the page table; the
+// decode kernel recovers logical positions per page (phys_to_logical, owner, seq_len), masks
+// slack, and with cfg.validate reports foreign pages as UnmappedPhysicalIndex.
+struct ConvertedMods {
+  MaskMod mask;
+  ScoreMod score;
+  std::shared_ptr<PageTable::Device> table;
+};
+inline ConvertedMods convert_mods(const MaskMod& mask, const ScoreMod& smod, const PageTable& pt,
+                                  cudaStream_t st = nullptr) {
+  return ConvertedMods{mask, smod, pt.to_device(st)};
+}
+// decode over a paged cache with converted mods (the reference passes cm.mask / cm.score).
+inline AttentionOutput decode(const DeviceTensor4& q_step, const PagedKVCache& cache, i64 offset,
+                              const ConvertedMods& cm, const BlockMask& physical_bm,
+                              const AttentionConfig& cfg = {}, OpCounters* counters = nullptr,
+                              cudaStream_t st = nullptr) {
+  return decode(q_step, cache.k_phys(), cache.v_phys(), offset, cm.mask, cm.score, physical_bm, cfg,
+                &cm.table->c, counters, st);
 }
 
 }  // namespace flexattn

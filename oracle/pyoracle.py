@@ -597,3 +597,19 @@ def ref_time_fwd_bwd(q, k, v, dout, mask: Mask, score: Score, bs=128, scale=None
                                   C.c_int64(bs), C.c_int(1 if do_bwd else 0), C.byref(f), C.byref(b))
     _check(st, lib)
     return f.value, b.value
+
+
+def ref_counters(q, k, v, dout, mask: Mask, score: Score, bs=128, scale=None, gqa=1):
+    """OpCounters of the reference forward<float> and backward<float> (engine.hpp:21-32):
+    ((madds, mask_evals, score_evals) forward, (...) backward)."""
+    q, k, v, dout = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v, dout))
+    B, Hq, Hkv, Bkv, Lq, Lkv, D = _dims(q, k, gqa)
+    out = np.zeros(6, np.uint64)
+    lib = ref()
+    mc, sc = mask.c(), score.c()
+    ct = C.c_float
+    st = lib.ref_counters_f32(*[_p(x, ct) for x in (q, k, v, dout)], *_i64(B, Hq, Hkv, Bkv, Lq, Lkv, D),
+                              C.c_double(scale or 0.0), C.c_int64(gqa), C.byref(sc), C.byref(mc),
+                              C.c_int64(bs), _p(out, C.c_uint64))
+    _check(st, lib)
+    return tuple(int(x) for x in out[:3]), tuple(int(x) for x in out[3:])

@@ -474,3 +474,31 @@ extern "C" int ref_time_fwd_bwd_f32(const float* q, const float* k, const float*
     return status_of(e);
   }
 }
+
+// OpCounters of the reference forward and backward (engine.hpp:21-32) on one problem:
+// out6 = {fwd madds, fwd mask_evals, fwd score_evals, bwd madds, bwd mask_evals, bwd score_evals}.
+extern "C" int ref_counters_f32(const float* q, const float* k, const float* v, const float* dout,
+                                int64_t B, int64_t Hq, int64_t Hkv, int64_t Bkv, int64_t Lq, int64_t Lkv,
+                                int64_t D, double scale, int64_t gqa, const RefScore* s, const RefMask* m,
+                                int64_t bs, uint64_t* out6) {
+  try {
+    AttentionConfig cfg;
+    if (scale > 0) cfg.scale = scale;
+    cfg.gqa_group = gqa;
+    cfg.block_size_q = cfg.block_size_kv = bs;
+    const auto bm = create_block_mask(make_mask(*m), 1, 1, Lq, Lkv, bs, bs);
+    const auto bm_t = transpose(bm);
+    const auto qt = tensor_from(q, B, Hq, Lq, D);
+    const auto kt = tensor_from(k, Bkv, Hkv, Lkv, D);
+    const auto vt = tensor_from(v, Bkv, Hkv, Lkv, D);
+    const auto smod = make_score(*s);
+    OpCounters cf, cb;
+    const auto fwd = forward(qt, kt, vt, smod, bm, cfg, &cf);
+    backward(qt, kt, vt, fwd, tensor_from(dout, B, Hq, Lq, D), smod, bm, bm_t, cfg, &cb);
+    const uint64_t v6[6] = {cf.madds, cf.mask_evals, cf.score_evals, cb.madds, cb.mask_evals, cb.score_evals};
+    std::copy(v6, v6 + 6, out6);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}

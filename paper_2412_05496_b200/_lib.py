@@ -48,13 +48,21 @@ class PageTableC(C.Structure):
     _fields_ = [("batches", C.c_int64), ("max_logical_pages", C.c_int64),
                 ("num_physical_pages", C.c_int64), ("page_size", C.c_int64),
                 ("table", C.c_void_p), ("phys_to_logical", C.c_void_p), ("owner", C.c_void_p),
-                ("seq_len", C.c_void_p)]
+                ("seq_len", C.c_void_p), ("max_seq_len", C.c_int64)]
+
+
+class OpCountersC(C.Structure):
+    _fields_ = [("madds", C.c_uint64), ("mask_evals", C.c_uint64), ("score_evals", C.c_uint64)]
+
+
+FA_FLAG_VALIDATE, FA_FLAG_DETERMINISTIC = 1, 2
 
 
 class FwdArgs(C.Structure):
     _fields_ = [("q", TensorC), ("k", TensorC), ("v", TensorC), ("out", TensorC),
                 ("lse", C.c_void_p), ("bm", C.POINTER(BlockMaskC)), ("mask", MaskDesc),
-                ("score", ScoreDesc), ("scale", C.c_double), ("gqa_group", C.c_int64)]
+                ("score", ScoreDesc), ("scale", C.c_double), ("gqa_group", C.c_int64),
+                ("flags", C.c_uint32), ("_pad1", C.c_int32), ("counters", C.POINTER(OpCountersC))]
 
 
 class BwdArgs(C.Structure):
@@ -62,7 +70,9 @@ class BwdArgs(C.Structure):
                 ("d_out", TensorC), ("lse", C.c_void_p), ("dq", TensorC), ("dk", TensorC),
                 ("dv", TensorC), ("bm", C.POINTER(BlockMaskC)), ("mask", MaskDesc),
                 ("score", ScoreDesc), ("scale", C.c_double), ("gqa_group", C.c_int64),
-                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("flags", C.c_uint32), ("_pad1", C.c_int32), ("counters", C.POINTER(OpCountersC)),
+                ("phase_events", C.c_void_p * 4)]
 
 
 class DecodeArgs(C.Structure):
@@ -70,7 +80,8 @@ class DecodeArgs(C.Structure):
                 ("lse", C.c_void_p), ("bm", C.POINTER(BlockMaskC)), ("pt", C.POINTER(PageTableC)),
                 ("offset", C.c_int64), ("mask", MaskDesc), ("score", ScoreDesc),
                 ("scale", C.c_double), ("gqa_group", C.c_int64), ("num_splits", C.c_int32),
-                ("_pad", C.c_int32), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
+                ("_pad", C.c_int32), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("flags", C.c_uint32), ("_pad2", C.c_int32), ("counters", C.POINTER(OpCountersC))]
 
 
 # Every symbol include/flexattn_b200.h declares (checked by tests/test_boundary.py).
@@ -79,6 +90,7 @@ EXPORTS = [
     "fa_block_mask_geometry", "fa_create_block_mask", "fa_transpose_block_mask",
     "fa_convert_block_mask", "fa_flex_fwd", "fa_bwd_workspace_size", "fa_flex_bwd",
     "fa_decode_workspace_size", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
+    "fa_check_finite",
 ]
 
 _lib = None
@@ -116,9 +128,10 @@ def load():
     lib.fa_fill_uniform.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]
     lib.fa_paged_write.argtypes = [C.POINTER(TensorC), C.POINTER(PageTableC), C.POINTER(TensorC),
                                    C.c_void_p]
+    lib.fa_check_finite.argtypes = [C.POINTER(TensorC), C.POINTER(C.c_char_p), C.c_int32, C.c_void_p]
     for fn in ("fa_create_block_mask", "fa_transpose_block_mask", "fa_convert_block_mask",
                "fa_flex_fwd", "fa_flex_bwd", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
-               "fa_block_mask_geometry"):
+               "fa_block_mask_geometry", "fa_check_finite"):
         getattr(lib, fn).restype = C.c_int32
     _lib = lib
     return lib

@@ -24,8 +24,8 @@ from typing import Optional, Sequence
 import torch
 
 from . import _lib
-from ._lib import (FA_BF16, FA_F32, BlockMaskC, BwdArgs, DecodeArgs, FwdArgs, MaskDesc,
-                   PageTableC, ScoreDesc, TensorC)
+from ._lib import (FA_BF16, FA_F32, FA_FLAG_DETERMINISTIC, FA_FLAG_VALIDATE, BlockMaskC, BwdArgs,
+                   DecodeArgs, FwdArgs, MaskDesc, OpCountersC, PageTableC, ScoreDesc, TensorC)
 
 # ---------------------------------------------------------------- errors (errors.hpp:11-101)
 
@@ -513,6 +513,35 @@ def _scale(cfg: AttentionConfig) -> float:
 
 
 @dataclass
+class OpCounters:
+    """OpCounters (engine.hpp:21-32), computed on the device from the BlockMask and the mask:
+    mask_evals and score_evals exactly as the reference counts them; madds without the
+    data-dependent accumulator-rescale term (see fa_op_counters in include/flexattn_b200.h).
+    Calls add into it, like the reference's ``*counters += worker counters``."""
+    madds: int = 0
+    mask_evals: int = 0
+    score_evals: int = 0
+
+    def _add(self, c: OpCountersC):
+        self.madds += int(c.madds)
+        self.mask_evals += int(c.mask_evals)
+        self.score_evals += int(c.score_evals)
+
+
+def check_finite(*named_tensors) -> None:
+    """validate_inputs' finiteness scan (validate.hpp:36-38) on the device: raises NonFiniteInput
+    naming the first tensor holding NaN/inf. ``named_tensors`` are (name, tensor) pairs."""
+    n = len(named_tensors)
+    arr = (TensorC * max(n, 1))()
+    names = (C.c_char_p * max(n, 1))()
+    for i, (name, t) in enumerate(named_tensors):
+        arr[i] = _tensor(t, name)
+        names[i] = name.encode()
+    with torch.cuda.device(named_tensors[0][1].device if n else torch.cuda.current_device()):
+        _check(_lib.load().fa_check_finite(arr, names, n, C.c_void_p(_stream())))
+
+
+@dataclass
 class AttentionOutput:
     """engine.hpp:38-46: out (B,H,L,D) and lse (B,H,L) natural log."""
     out: torch.Tensor
@@ -537,9 +566,12 @@ def _prep_mods(smod: ScoreMod, bm: BlockMask, mask: Optional[MaskMod]):
 
 def forward(q, k, v, smod: ScoreMod, bm: BlockMask, cfg: Optional[AttentionConfig] = None,
             mask: Optional[MaskMod] = None, out: Optional[torch.Tensor] = None,
-            lse: Optional[torch.Tensor] = None) -> AttentionOutput:
+            lse: Optional[torch.Tensor] = None, counters: Optional[OpCounters] = None,
+            validate: bool = False) -> AttentionOutput:
     """forward<Real> (engine.cpp:46-172) on the GPU: bf16 -> tcgen05 kernel (bs 128,
-    D 64/128), otherwise the fp32 CUDA-core kernel."""
+    D 64/128), otherwise the fp32 CUDA-core kernel. ``counters`` (OpCounters) and
+    ``validate=True`` (the reference's NaN/inf scan of q/k/v -> NonFiniteInput) each cost a
+    device pass and a stream synchronisation."""
     cfg = cfg or AttentionConfig()
     cfg.validate()
     m = _prep_mods(smod, bm, mask)
@@ -555,16 +587,26 @@ def forward(q, k, v, smod: ScoreMod, bm: BlockMask, cfg: Optional[AttentionConfi
     a.bm = C.pointer(cbm)
     a.mask, a.score = m.desc(q.device), smod.desc(q.device)
     a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
+    a.flags = FA_FLAG_VALIDATE if validate else 0
+    cc = OpCountersC()
+    if counters is not None:
+        a.counters = C.pointer(cc)
     with torch.cuda.device(q.device):
         _check(_lib.load().fa_flex_fwd(C.byref(a), C.c_void_p(_stream())))
+    if counters is not None:
+        counters._add(cc)
     return AttentionOutput(out, lse)
 
 
 def backward(q, k, v, fwd: AttentionOutput, d_out, smod: ScoreMod, bm: BlockMask,
              bm_t: Optional[BlockMask] = None, cfg: Optional[AttentionConfig] = None,
-             mask: Optional[MaskMod] = None) -> Gradients:
+             mask: Optional[MaskMod] = None, counters: Optional[OpCounters] = None,
+             validate: bool = False, deterministic: bool = False, phase_events=None) -> Gradients:
     """backward<Real> (engine.cpp:174-401): dQ/dK/dV through score_mod'. ``bm_t`` is
-    accepted for signature parity; the q-side arrays live in ``bm``."""
+    accepted for signature parity; the q-side arrays live in ``bm``. ``deterministic=True``
+    orders the dQ additions so the gradients are bitwise reproducible run to run (the default
+    tensor-core path adds dQ partial sums in arrival order; dK/dV are reproducible either way).
+    ``phase_events``: optional 4 torch.cuda.Event recorded around the kernels (timing)."""
     cfg = cfg or AttentionConfig()
     cfg.validate()
     m = _prep_mods(smod, bm, mask)
@@ -589,8 +631,19 @@ def backward(q, k, v, fwd: AttentionOutput, d_out, smod: ScoreMod, bm: BlockMask
     a.mask, a.score = m.desc(q.device), smod.desc(q.device)
     a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
     a.workspace, a.workspace_bytes = work.data_ptr(), ws
+    a.flags = (FA_FLAG_VALIDATE if validate else 0) | (FA_FLAG_DETERMINISTIC if deterministic else 0)
+    cc = OpCountersC()
+    if counters is not None:
+        a.counters = C.pointer(cc)
+    if phase_events is not None:
+        for i, ev in enumerate(phase_events):
+            if not ev.cuda_event:  # torch creates its events lazily, on the first record
+                ev.record()
+            a.phase_events[i] = ev.cuda_event
     with torch.cuda.device(q.device):
         _check(lib.fa_flex_bwd(C.byref(a), C.c_void_p(_stream())))
+    if counters is not None:
+        counters._add(cc)
     return Gradients(dq, dk, dv)
 
 
@@ -608,7 +661,8 @@ def _workspace(device, nbytes) -> torch.Tensor:
 
 def decode(q_step, k_cache, v_cache, offset: int, mask: MaskMod, smod: ScoreMod, bm: BlockMask,
            cfg: Optional[AttentionConfig] = None, page_table: Optional["PageTable"] = None,
-           num_splits: int = 0) -> AttentionOutput:
+           num_splits: int = 0, counters: Optional[OpCounters] = None,
+           validate: bool = False) -> AttentionOutput:
     """decode (engine.cpp:403-427): q_step rows sit at [offset, offset+n_new). ``mask``/``smod``
     speak absolute positions; ``bm`` describes the shifted mask at q_len = n_new (converted to
     physical pages when ``page_table`` is given)."""
@@ -638,8 +692,14 @@ def decode(q_step, k_cache, v_cache, offset: int, mask: MaskMod, smod: ScoreMod,
     a.scale, a.gqa_group = _scale(cfg), cfg.gqa_group
     a.num_splits = int(num_splits)
     a.workspace, a.workspace_bytes = work.data_ptr(), ws
+    a.flags = FA_FLAG_VALIDATE if validate else 0
+    cc = OpCountersC()
+    if counters is not None:
+        a.counters = C.pointer(cc)
     with torch.cuda.device(q_step.device):
         _check(lib.fa_flex_decode(C.byref(a), C.c_void_p(_stream())))
+    if counters is not None:
+        counters._add(cc)
     return AttentionOutput(out, lse)
 
 
@@ -702,6 +762,7 @@ class PageTable:
         s.num_physical_pages, s.page_size = self.num_physical_pages, self.page_size
         s.table, s.phys_to_logical, s.owner, s.seq_len = (t.data_ptr(), p2l.data_ptr(),
                                                            own.data_ptr(), sl.data_ptr())
+        s.max_seq_len = max(self.seq_len) if self.seq_len else 0
         return s
 
 

@@ -19,7 +19,7 @@ fa_status launch_bwd_sm100(const AttnGeom& g, const void* q, const void* k, cons
                            const void* o, const float* lse, const void* dout, void* dq, void* dk,
                            void* dv, const BmView& bm, const BmView& bmt, const MaskParams& mp,
                            int mkind, const ScoreParams& sp, int skind, void* workspace,
-                           cudaStream_t st);
+                           const BwdOptions& opt, cudaStream_t st);
 
 namespace {
 
@@ -247,10 +247,11 @@ fa_status launch_bwd(const AttnGeom& g, const void* q, const void* k, const void
                      const void* o, const float* lse, const void* dout, void* dq, void* dk,
                      void* dv, int dtype, const BmView& bm, const BmView& bmt,
                      const MaskParams& mp, int mkind, const ScoreParams& sp, int skind,
-                     void* workspace, cudaStream_t st) {
+                     void* workspace, const BwdOptions& opt, cudaStream_t st) {
   if (dtype == FA_BF16 && bwd_sm100_supported(g))
     return launch_bwd_sm100(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind,
-                            workspace, st);
+                            workspace, opt, st);
+  // the CUDA-core passes are deterministic by construction (separate dq pass, no atomics)
   // workspace layout (fa_bwd_workspace_size): [dq_acc | delta | lse2]; delta only here
   const size_t rows = (size_t)g.B * g.Hq * g.Lq;
   const size_t off = ((rows * g.D * 4) + 255) & ~size_t(255);

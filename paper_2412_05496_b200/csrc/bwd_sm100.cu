@@ -67,6 +67,12 @@ struct BwdParams {
   const int32_t* q_idx;
   const int32_t* fq_num;
   const int32_t* fq_idx;
+  const int32_t* kv_num;   // kv side (deterministic mode: rank of a kv block in a q row's list)
+  const int32_t* kv_idx;
+  const int32_t* fkv_num;
+  const int32_t* fkv_idx;
+  int* turn;           // deterministic mode: per (b*Hq + h, q block) count of finished dQ adds
+  int deterministic;
   const float* lse2;   // (B*Hq, Lq_pad): cterm, see bwd_preprocess_kernel
   const float* delta;  // (B*Hq, Lq_pad)
   float* dq_acc;       // (B*Hq, Lq, D) fp32
@@ -204,6 +210,44 @@ __device__ __forceinline__ int count_tasks(const BwdParams& p, const KvItem& it)
   return total;
 }
 
+// ---- deterministic dQ (FA_FLAG_DETERMINISTIC) ----
+// The contributions to dQ of q block r of (b, h) come from the kv blocks c of r's kv-side lists,
+// one item each. Each of the 4 reduction warps of the item of rank k (k = number of listed kv
+// blocks < c) waits until all 4 warps of rank k-1 have their TMA reduce-adds complete, so every
+// fp32 element of the accumulator receives its adds in ascending-c order. Waits only point to
+// lower items, and in this mode every item is claimed by a running CTA: no deadlock.
+__device__ __forceinline__ int* det_wait_turn(const BwdParams& p, const KvItem& it, int b, int h, int r,
+                                              int lane) {
+  const int mb = p.bm_b == 1 ? 0 : b, mh = p.bm_h == 1 ? 0 : h;
+  const long long slot = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r;
+  const int np = __ldg(p.kv_num + slot), nf = __ldg(p.fkv_num + slot);
+  int rank = 0;
+  for (int i = lane; i < np + nf; i += 32) {
+    const int c = i < np ? __ldg(p.kv_idx + slot * p.cols + i) : __ldg(p.fkv_idx + slot * p.cols + (i - np));
+    rank += __popc(__ballot_sync(__activemask(), c < it.c));
+  }
+  rank = __shfl_sync(0xffffffffu, rank, 0);
+  int* turn = p.turn + static_cast<long long>(b * p.Hq + h) * p.rows + r;
+  if (lane == 0) {
+    const int want = 4 * rank;
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(turn) : "memory");
+    } while (v < want);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+  return turn;
+}
+__device__ __forceinline__ void det_finish_turn(int* turn, int lane) {
+  if (lane == 0) {
+    bulk_wait_group<0>();  // this warp's reduce-adds have been performed
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(turn) : "memory");
+  }
+  __syncwarp();
+}
+
 template <int D, class MaskT, class ScoreT>
 __global__ void __launch_bounds__(kThreads, 1)
     flex_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -282,8 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===================== TMA producer =====================
       int blk = 0;
       for (int n = 0;; ++n) {
-        const int item = n == 0 ? static_cast<int>(blockIdx.x)
-                                : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
+        // deterministic mode claims every item from the counter, so an item is only ever
+        // owned by a CTA that is running (the ordered dQ adds wait on lower items only)
+        const int item = p.deterministic ? atomicAdd(p.work_counter, 1)
+                         : n == 0        ? static_cast<int>(blockIdx.x)
+                                         : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
         const int buf = n & 1;
         mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
         sm.uitem[buf] = item < p.num_items ? item : -1;
@@ -692,6 +739,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (C::kTmaReduce) {
             // four 32 (q) x 32 (d) fp32 tiles per warp: st.shared rows of 128 B (lane = d),
             // then one TMA reduce-add each (rows past Q_LEN are clipped by the tensor map)
+            int* turn = nullptr;
+            if (p.deterministic) turn = det_wait_turn(p, it, b, h, r, lane);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4, ++stage_it) {
               float* stg = sm.dq_stage[wq][stage_it & 1];
@@ -706,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bulk_commit_group();
               }
             }
+            if (turn != nullptr) det_finish_turn(turn, lane);
           } else {
           // per q row the warp's 32 lanes add 32 consecutive floats: one 128-byte line per red
           const int d = wq * 32 + lane;
@@ -732,6 +782,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&sm.dq_empty);
           if constexpr (C::kTmaReduce) {
             // one 32 (q) x D fp32 tile per warp (row per lane; bank conflicts accepted at D=64)
+            int* turn = nullptr;
+            if (p.deterministic) turn = det_wait_turn(p, it, b, h, r, lane);
             float* stg = sm.dq_stage[wq][stage_it & 1];
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
@@ -750,6 +802,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_reduce_add_3d(&tmDQ, stg, 0, r * kTile + wq * 32, b * p.Hq + h);
               bulk_commit_group();
             }
+            if (turn != nullptr) det_finish_turn(turn, lane);
             ++stage_it;
           } else {
             const int qrow = r * kTile + wq * 32 + lane;
@@ -821,7 +874,8 @@ template <class ScoreT>
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad, int D, float scale, ScoreT score,
-    float* __restrict__ cterm, float* __restrict__ delta, float* __restrict__ dq_acc) {
+    float* __restrict__ cterm, float* __restrict__ delta, float* __restrict__ dq_acc,
+    int* __restrict__ turn, int* __restrict__ dout_bad) {
   // 8 lanes per row: each lane reads D/8 contiguous bf16 of O and dO with 16-byte loads and
   // zeroes its D/8 floats of the dQ accumulator (the memset of the fp32 workspace, fused)
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
@@ -829,6 +883,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
   if (row >= (long long)BH * Lq_pad) return;
   const int q = (int)(row % Lq_pad);
   const long long bh = row / Lq_pad;
+  if (turn != nullptr && sub == 0 && (q & (kTile - 1)) == 0) turn[bh * (Lq_pad / kTile) + q / kTile] = 0;
   if (q >= Lq) {
     if (sub == 0) {
       cterm[row] = -INFINITY;
@@ -841,8 +896,17 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
   const uint4* d4 = reinterpret_cast<const uint4*>(dout + src);
   float4* z4 = reinterpret_cast<float4*>(dq_acc + src);
   float a = 0.f;
+  bool bad = false;
   for (int v = 0; v < D / 64; ++v) {
     const uint4 x = __ldg(o4 + v), y = __ldg(d4 + v);
+    if (dout_bad != nullptr) {  // d_out finiteness (engine.cpp:196), folded into this read
+      const uint32_t w[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t t = w[e] & 0x7f807f80u;
+        bad |= (t & 0xffffu) == 0x7f80u || (t >> 16) == 0x7f80u;
+      }
+    }
     const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
     const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
 #pragma unroll
@@ -853,6 +917,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     z4[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
     z4[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  if (bad) atomicOr(dout_bad, 1);
   a += __shfl_xor_sync(0xffffffffu, a, 4);
   a += __shfl_xor_sync(0xffffffffu, a, 2);
   a += __shfl_xor_sync(0xffffffffu, a, 1);
@@ -876,8 +941,9 @@ __global__ void dq_convert_kernel(const float4* __restrict__ acc, uint4* __restr
 
 template <int D, class MaskT, class ScoreT>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
-              const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bmt,
-              MaskT mask, ScoreT score, void* workspace, cudaStream_t st) {
+              const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
+              const BmView& bmt, MaskT mask, ScoreT score, void* workspace, const BwdOptions& opt,
+              cudaStream_t st) {
   const int Lq_pad = (g.Lq + kTile - 1) / kTile * kTile;
   const long long rows = (long long)g.B * g.Hq * g.Lq;
   const long long prow = (long long)g.B * g.Hq * Lq_pad;
@@ -886,10 +952,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
+  const bool det = (opt.flags & FA_FLAG_DETERMINISTIC) != 0;
+  int* turn = det ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
+  if (opt.events[0]) FA_CHECK_CUDA(cudaEventRecord(opt.events[0], st));
   // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
   bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
-      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc);
+      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc, turn, opt.dout_nonfinite);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
@@ -906,6 +975,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.Lq_pad = Lq_pad;
   p.bm_b = g.bm_b; p.bm_h = g.bm_h; p.rows = g.rows; p.cols = g.cols;
   p.q_num = bmt.kv_num; p.q_idx = bmt.kv_idx; p.fq_num = bmt.full_num; p.fq_idx = bmt.full_idx;
+  p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.fkv_num = bm.full_num; p.fkv_idx = bm.full_idx;
+  p.turn = turn;
+  p.deterministic = det ? 1 : 0;
   p.lse2 = lse2; p.delta = delta; p.dq_acc = dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(dk);
   p.dv = static_cast<__nv_bfloat16*>(dv);
@@ -924,6 +996,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
+  if (opt.events[1]) FA_CHECK_CUDA(cudaEventRecord(opt.events[1], st));
   if (grid > 0) {
     kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, mdo, mdq, p, mask, score);
     count_launch();
@@ -976,35 +1049,39 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
               acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, acc[9] / cnt, acc[10] / cnt, acc[11] / cnt);
   }
   const long long n8 = rows * D / 8;
+  if (opt.events[2]) FA_CHECK_CUDA(cudaEventRecord(opt.events[2], st));
   dq_convert_kernel<<<(unsigned)std::min<long long>((n8 + 255) / 256, 148LL * 16), 256, 0, st>>>(
       reinterpret_cast<const float4*>(dq_acc), static_cast<uint4*>(dq), n8);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
+  if (opt.events[3]) FA_CHECK_CUDA(cudaEventRecord(opt.events[3], st));
   return FA_OK;
 }
 
 template <int D, class ScoreT>
 fa_status by_mask(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
-                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bmt,
-                  const MaskParams& mp, int mk, ScoreT s, void* ws, cudaStream_t st) {
+                  const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
+                  const BmView& bmt, const MaskParams& mp, int mk, ScoreT s, void* ws,
+                  const BwdOptions& opt, cudaStream_t st) {
   switch (mk) {
-    case kMaskNoop: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, MaskFn<kMaskNoop>{mp}, s, ws, st);
-    case kMaskCausalOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, MaskFn<kMaskCausalOnly>{mp}, s, ws, st);
-    case kMaskSlidingOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, MaskFn<kMaskSlidingOnly>{mp}, s, ws, st);
-    case kMaskDocCausal: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, MaskFn<kMaskDocCausal>{mp}, s, ws, st);
-    default: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, MaskFn<kMaskDynamic>{mp}, s, ws, st);
+    case kMaskNoop: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskNoop>{mp}, s, ws, opt, st);
+    case kMaskCausalOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskCausalOnly>{mp}, s, ws, opt, st);
+    case kMaskSlidingOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskSlidingOnly>{mp}, s, ws, opt, st);
+    case kMaskDocCausal: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskDocCausal>{mp}, s, ws, opt, st);
+    default: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
   }
 }
 
 template <int D>
 fa_status by_score(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
-                   const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bmt,
-                   const MaskParams& mp, int mk, const ScoreParams& sp, int sk, void* ws, cudaStream_t st) {
+                   const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
+                   const BmView& bmt, const MaskParams& mp, int mk, const ScoreParams& sp, int sk,
+                   void* ws, const BwdOptions& opt, cudaStream_t st) {
   switch (sk) {
-    case 0: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mk, ScoreFn<0>{sp}, ws, st);
-    case 1: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mk, ScoreFn<1>{sp}, ws, st);
-    case 2: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mk, ScoreFn<2>{sp}, ws, st);
-    default: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mk, ScoreFn<3>{sp}, ws, st);
+    case 0: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<0>{sp}, ws, opt, st);
+    case 1: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<1>{sp}, ws, opt, st);
+    case 2: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<2>{sp}, ws, opt, st);
+    default: return by_mask<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<3>{sp}, ws, opt, st);
   }
 }
 
@@ -1018,11 +1095,10 @@ fa_status launch_bwd_sm100(const AttnGeom& g, const void* q, const void* k, cons
                            const void* o, const float* lse, const void* dout, void* dq, void* dk,
                            void* dv, const BmView& bm, const BmView& bmt, const MaskParams& mp,
                            int mkind, const ScoreParams& sp, int skind, void* workspace,
-                           cudaStream_t st) {
-  (void)bm;
+                           const BwdOptions& opt, cudaStream_t st) {
   if (g.D == 128)
-    return by_score<128>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mkind, sp, skind, workspace, st);
-  return by_score<64>(g, q, k, v, o, lse, dout, dq, dk, dv, bmt, mp, mkind, sp, skind, workspace, st);
+    return by_score<128>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, workspace, opt, st);
+  return by_score<64>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, workspace, opt, st);
 }
 
 }  // namespace fa

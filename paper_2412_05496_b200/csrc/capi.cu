@@ -223,7 +223,7 @@ BmView kv_view(const fa_block_mask* bm) {
 extern "C" {
 
 const char* fa_last_error(void) { return g_last_error.c_str(); }
-int32_t fa_abi_version(void) { return 2; }  // v2: fa_mask_desc or_terms / natten / remap
+int32_t fa_abi_version(void) { return 3; }  // v3: flags, counters, phase events, fa_check_finite
 uint64_t fa_launch_count(void) { return g_launches.load(); }
 
 const char* fa_status_name(fa_status s) {
@@ -263,11 +263,20 @@ fa_status fa_flex_fwd(const fa_fwd_args* a, void* stream) {
   const ScoreParams sp = to_score_params(a->score);
   const int mk = mask_kind_of(a->mask);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  FA_REQUIRE(!(a->flags & ~uint32_t(FA_FLAG_VALIDATE)), FA_SHAPE_MISMATCH, "forward: unknown flags");
+  if (a->flags & FA_FLAG_VALIDATE) {  // validate_inputs (validate.hpp:36-38)
+    const fa_tensor ts[3] = {a->q, a->k, a->v};
+    const char* names[3] = {"q", "k", "v"};
+    if ((s = check_finite_list(ts, names, 3, st)) != FA_OK) return s;
+  }
   if (a->q.dtype == FA_BF16 && fwd_sm100_supported(g))
-    return launch_fwd_sm100(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, kv_view(a->bm),
-                            mp, mk, sp, (int)a->score.terms, st);
-  return launch_fwd_simt(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->q.dtype,
-                         kv_view(a->bm), mp, mk, sp, (int)a->score.terms, st);
+    s = launch_fwd_sm100(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, kv_view(a->bm),
+                         mp, mk, sp, (int)a->score.terms, st);
+  else
+    s = launch_fwd_simt(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->q.dtype,
+                        kv_view(a->bm), mp, mk, sp, (int)a->score.terms, st);
+  if (s != FA_OK || a->counters == nullptr) return s;
+  return compute_counters(g, kv_view(a->bm), mp, mk, nullptr, g.Lkv, kPassForward, a->counters, st);
 }
 
 size_t fa_bwd_workspace_size(int64_t batch, int64_t heads, int64_t q_len, int64_t dim) {
@@ -275,7 +284,9 @@ size_t fa_bwd_workspace_size(int64_t batch, int64_t heads, int64_t q_len, int64_
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t rows = static_cast<size_t>(batch * heads * q_len);
   const size_t prow = static_cast<size_t>(batch * heads * ((q_len + 127) / 128 * 128));
-  return al(rows * dim * 4) + al(prow * 4) + al(prow * 4);
+  const size_t qblocks = static_cast<size_t>(batch * heads * ((q_len + 127) / 128));
+  // + per-(b, h, q block) turn counters of the deterministic dQ order
+  return al(rows * dim * 4) + al(prow * 4) + al(prow * 4) + al(qblocks * 4);
 }
 
 fa_status fa_flex_bwd(const fa_bwd_args* a, void* stream) {
@@ -307,14 +318,42 @@ fa_status fa_flex_bwd(const fa_bwd_args* a, void* stream) {
   FA_REQUIRE(a->workspace != nullptr &&
                  a->workspace_bytes >= fa_bwd_workspace_size(a->q.b, a->q.h, a->q.l, a->q.d),
              FA_SHAPE_MISMATCH, "backward: workspace too small");
+  FA_REQUIRE(!(a->flags & ~uint32_t(FA_FLAG_VALIDATE | FA_FLAG_DETERMINISTIC)), FA_SHAPE_MISMATCH,
+             "backward: unknown flags");
   const AttnGeom g = geom_of(a->q, a->k, a->bm, a->scale, a->gqa_group);
   const BmView bmt{a->bm->q_num_blocks, a->bm->q_indices, a->bm->full_q_num_blocks,
                    a->bm->full_q_indices};
-  return launch_bwd(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->d_out.data,
-                    a->dq.data, a->dk.data, a->dv.data, a->q.dtype, kv_view(a->bm), bmt,
-                    to_mask_params(a->mask), mask_kind_of(a->mask),
-                    to_score_params(a->score), (int)a->score.terms, a->workspace,
-                    static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool tc_path = a->q.dtype == FA_BF16 && bwd_sm100_supported(g);
+  BwdOptions opt;
+  opt.flags = a->flags;
+  for (int i = 0; i < 4; ++i) opt.events[i] = static_cast<cudaEvent_t>(a->phase_events[i]);
+  if (a->flags & FA_FLAG_VALIDATE) {
+    // q/k/v as validate_inputs; d_out (engine.cpp:196) is checked inside the tensor-core
+    // path's preprocess read of d_out, else scanned here
+    const fa_tensor ts[4] = {a->q, a->k, a->v, a->d_out};
+    const char* names[4] = {"q", "k", "v", "d_out"};
+    if ((s = check_finite_list(ts, names, tc_path ? 3 : 4, st)) != FA_OK) return s;
+    if (tc_path) {
+      opt.dout_nonfinite = scheduler_counter(kSlotFiniteErr, st);
+      FA_REQUIRE(opt.dout_nonfinite != nullptr, FA_CUDA_ERROR, "backward: status word");
+      FA_CHECK_CUDA(cudaMemsetAsync(opt.dout_nonfinite, 0, sizeof(int), st));
+    }
+  }
+  const MaskParams mp = to_mask_params(a->mask);
+  const int mk = mask_kind_of(a->mask);
+  s = launch_bwd(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->d_out.data, a->dq.data,
+                 a->dk.data, a->dv.data, a->q.dtype, kv_view(a->bm), bmt, mp, mk,
+                 to_score_params(a->score), (int)a->score.terms, a->workspace, opt, st);
+  if (s != FA_OK) return s;
+  if (opt.dout_nonfinite != nullptr) {
+    int bad = 0;
+    FA_CHECK_CUDA(cudaMemcpyAsync(&bad, opt.dout_nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FA_CHECK_CUDA(cudaStreamSynchronize(st));
+    FA_REQUIRE(bad == 0, FA_NON_FINITE_INPUT, "backward: d_out contains NaN or inf");
+  }
+  if (a->counters == nullptr) return FA_OK;
+  return compute_counters(g, kv_view(a->bm), mp, mk, nullptr, g.Lkv, kPassBackward, a->counters, st);
 }
 
 size_t fa_decode_workspace_size(int64_t batch, int64_t heads, int64_t n_new, int64_t dim,
@@ -361,7 +400,11 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
                    a->bm->full_kv_indices,
                FA_BLOCK_MASK_MISMATCH, "decode: block mask kv-side arrays missing");
     logical_kv = pt->max_logical_pages * pt->page_size;
+    FA_REQUIRE(pt->max_seq_len >= 0 && pt->max_seq_len <= logical_kv, FA_SHAPE_MISMATCH,
+               "decode: page table max_seq_len outside [0, max_logical_pages * page_size]");
   }
+  // kv positions the mask can be evaluated at (the paged kernel also stops at each seq_len)
+  const int64_t mask_kv = (a->pt && a->pt->max_seq_len > 0) ? a->pt->max_seq_len : logical_kv;
   // engine.cpp:410-414
   FA_REQUIRE(a->offset >= 0 && a->offset + n_new <= logical_kv, FA_OFFSET_OUT_OF_RANGE,
              "decode: rows [" + std::to_string(a->offset) + ", " + std::to_string(a->offset + n_new) +
@@ -374,19 +417,28 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
   m.q_offset += a->offset;  // offset_mask / offset_score (mask_library.cpp:106-119)
   sc.q_offset += a->offset;
   // the kernels evaluate the mask at logical kv positions up to logical_kv - 1
-  if ((s = check_mods(m, sc, a->q.h, n_new, logical_kv))) return s;
+  if ((s = check_mods(m, sc, a->q.h, n_new, mask_kv))) return s;
+  FA_REQUIRE(!(a->flags & ~uint32_t(FA_FLAG_VALIDATE)), FA_SHAPE_MISMATCH, "decode: unknown flags");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (a->flags & FA_FLAG_VALIDATE) {  // decode -> forward_impl -> validate_inputs
+    const fa_tensor ts[3] = {a->q, a->k_cache, a->v_cache};
+    const char* names[3] = {"q", "k", "v"};
+    if ((s = check_finite_list(ts, names, 3, st)) != FA_OK) return s;
+  }
   if (a->q.dtype == FA_F32) {
     // decode<float> is forward_impl over the shifted mask (engine.cpp:403-427): the fp32
     // CUDA-core forward with q_offset applied to the mask and score terms
     const AttnGeom ga = geom_of(a->q, a->k_cache, a->bm, a->scale, a->gqa_group);
-    return launch_fwd_simt(ga, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse, FA_F32,
-                           kv_view(a->bm), to_mask_params(m), mask_kind_of(m), to_score_params(sc),
-                           (int)sc.terms, static_cast<cudaStream_t>(stream));
+    s = launch_fwd_simt(ga, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse, FA_F32,
+                        kv_view(a->bm), to_mask_params(m), mask_kind_of(m), to_score_params(sc),
+                        (int)sc.terms, st);
+    if (s != FA_OK || a->counters == nullptr) return s;
+    return compute_counters(ga, kv_view(a->bm), to_mask_params(m), mask_kind_of(m), nullptr, (int)ga.Lkv,
+                            kPassForward, a->counters, st);
   }
   DecodeGeom g{};
   g.a = geom_of(a->q, a->k_cache, a->bm, a->scale, a->gqa_group);
-  g.logical_kv = (int)(a->pt ? logical_kv : a->k_cache.l);
-  if (a->pt) g.logical_kv = (int)std::min<int64_t>(logical_kv, a->pt->max_logical_pages * a->pt->page_size);
+  g.logical_kv = (int)mask_kv;
   int splits = a->num_splits;
   if (splits <= 0) {
     const int64_t rows_total = a->q.b * a->q.h * n_new;
@@ -405,11 +457,26 @@ fa_status fa_flex_decode(const fa_decode_args* a, void* stream) {
     pv.seq_len = a->pt->seq_len;
     pv.page_size = (int)a->pt->page_size;
     pv.enabled = 1;
+    if (a->flags & FA_FLAG_VALIDATE) {  // foreign pages -> UnmappedPhysicalIndex (paged_kv.cpp:265-269)
+      pv.foreign = scheduler_counter(kSlotConvertErr, st);
+      FA_REQUIRE(pv.foreign != nullptr, FA_CUDA_ERROR, "decode: status word");
+      FA_CHECK_CUDA(cudaMemsetAsync(pv.foreign, 0, sizeof(int), st));
+    }
   }
-  return launch_decode(g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse,
-                       kv_view(a->bm), pv, to_mask_params(m), mask_kind_of(m),
-                       to_score_params(sc), (int)sc.terms, a->workspace,
-                       static_cast<cudaStream_t>(stream));
+  const MaskParams mp = to_mask_params(m);
+  const int mk = mask_kind_of(m);
+  s = launch_decode(g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse, kv_view(a->bm),
+                    pv, mp, mk, to_score_params(sc), (int)sc.terms, a->workspace, st);
+  if (s != FA_OK) return s;
+  if (pv.foreign != nullptr) {
+    int bad = 0;
+    FA_CHECK_CUDA(cudaMemcpyAsync(&bad, pv.foreign, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FA_CHECK_CUDA(cudaStreamSynchronize(st));
+    FA_REQUIRE(bad == 0, FA_UNMAPPED_PHYSICAL_INDEX,
+               "converted modifier: a visited physical page is not mapped for its batch element");
+  }
+  if (a->counters == nullptr) return FA_OK;
+  return compute_counters(g.a, kv_view(a->bm), mp, mk, &pv, g.logical_kv, kPassForward, a->counters, st);
 }
 
 }  // extern "C"

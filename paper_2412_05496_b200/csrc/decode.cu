@@ -49,6 +49,7 @@ struct DecParams {
   const int32_t* p2l;
   const int32_t* owner;
   const int32_t* seq_len;
+  int* foreign;  // optional: set when a visited page is foreign to the row's batch element
   int paged, logical_kv;
   int splits;
   float scale;
@@ -129,6 +130,9 @@ __global__ void __launch_bounds__(128, 1) decode_kernel(DecParams p, MaskT mask,
       lpage = __ldg(p.p2l + c);
       own = __ldg(p.owner + c);
       seq = min(__ldg(p.seq_len + b), p.logical_kv);
+      // convert_mods throws UnmappedPhysicalIndex on such a page (paged_kv.cpp:265-269); here
+      // it is masked and reported through the status word when the caller validates
+      if (p.foreign != nullptr && tid == 0 && (own != b || lpage < 0)) atomicOr(p.foreign, 1);
     }
     const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(sm.kv[s][0]);
     const __nv_bfloat16* vs = reinterpret_cast<const __nv_bfloat16*>(sm.kv[s][1]);
@@ -338,6 +342,7 @@ fa_status launch_decode(const DecodeGeom& g, const void* q, const void* k, const
   p.bs_q = a.bs_q; p.bs_kv = a.bs_kv;
   p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.full_num = bm.full_num; p.full_idx = bm.full_idx;
   p.p2l = pv.phys_to_logical; p.owner = pv.owner; p.seq_len = pv.seq_len; p.paged = pv.enabled;
+  p.foreign = pv.foreign;
   p.logical_kv = g.logical_kv;
   p.splits = g.num_splits;
   p.scale = a.scale;

@@ -77,6 +77,7 @@ struct PageView {
   const int32_t* seq_len;
   int page_size;
   int enabled;
+  int* foreign = nullptr;  // device word set when a visited page is not the row's batch element's
 };
 
 fa_status launch_decode(const DecodeGeom& g, const void* q, const void* k, const void* v, void* o,
@@ -84,11 +85,26 @@ fa_status launch_decode(const DecodeGeom& g, const void* q, const void* k, const
                         int mkind, const ScoreParams& sp, int skind, void* workspace,
                         cudaStream_t st);
 
+// OpCounters of one call (engine.hpp:21-32) from the BlockMask and the mask; synchronises `st`.
+enum { kPassForward = 0, kPassBackward = 1 };
+fa_status compute_counters(const AttnGeom& a, const BmView& bm, const MaskParams& mp, int mkind,
+                           const PageView* pv, int logical_kv, int pass, fa_op_counters* out,
+                           cudaStream_t st);
+// NaN/inf scan of n tensors (validate.hpp:36-38); synchronises `st`.
+fa_status check_finite_list(const fa_tensor* ts, const char* const* names, int n, cudaStream_t st);
+
+// Backward options beyond the tensors (ABI v3 fields of fa_bwd_args).
+struct BwdOptions {
+  uint32_t flags = 0;               // FA_FLAG_*
+  cudaEvent_t events[4] = {nullptr, nullptr, nullptr, nullptr};  // phase timing, may be null
+  int* dout_nonfinite = nullptr;    // device word set by the preprocess when d_out has NaN/inf
+};
+
 bool bwd_sm100_supported(const AttnGeom& g);
 fa_status launch_bwd(const AttnGeom& g, const void* q, const void* k, const void* v,
                      const void* o, const float* lse, const void* dout, void* dq, void* dk,
                      void* dv, int dtype, const BmView& bm, const BmView& bmt,
                      const MaskParams& mp, int mkind, const ScoreParams& sp, int skind,
-                     void* workspace, cudaStream_t st);
+                     void* workspace, const BwdOptions& opt, cudaStream_t st);
 
 }  // namespace fa

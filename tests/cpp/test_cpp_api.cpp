@@ -172,6 +172,104 @@ int main() {
     } catch (const BlockMaskMismatch&) { thrown = true; }
     EXPECT(thrown);
   }
+  // ---- OpCounters (test_engine.cpp:273-326) -----------------------------------------------------
+  {
+    const i64 L = 512, D = 64;
+    DeviceTensor4 q = random_tensor(701, 1, 1, L, D, DType::F32), k = random_tensor(702, 1, 1, L, D, DType::F32),
+                  v = random_tensor(703, 1, 1, L, D, DType::F32);
+    OpCounters causal_ops, dense_ops;
+    forward(q, k, v, noop_score(), create_block_mask(causal(), 1, 1, L, L), {}, &causal_ops);
+    forward(q, k, v, noop_score(), create_block_mask(noop_mask(), 1, 1, L, L), {}, &dense_ops);
+    EXPECT(causal_ops.mask_evals == 4ull * 128 * 128);
+    EXPECT(dense_ops.mask_evals == 0);
+    EXPECT(causal_ops.score_evals == std::uint64_t(L) * (L + 1) / 2);
+    EXPECT(dense_ops.score_evals == std::uint64_t(L) * L);
+    const double ratio = double(causal_ops.madds) / double(dense_ops.madds);
+    EXPECT(ratio > 0.40 && ratio <= 0.60);
+  }
+  // ---- validation: NonFiniteInput, deterministic backward ------------------------------------------
+  {
+    DeviceTensor4 q = random_tensor(11, 1, 2, 256, 128), k = random_tensor(12, 1, 2, 256, 128);
+    BlockMask bm = create_block_mask(causal(), 1, 1, 256, 256);
+    const uint16_t nan_bf16 = 0x7fc0;
+    check_cuda(cudaMemcpy(k.buf.as<uint16_t>() + 777, &nan_bf16, 2, cudaMemcpyHostToDevice), "poke");
+    AttentionConfig cfg;
+    cfg.validate = true;
+    bool thrown = false;
+    try { forward(q, k, q, noop_score(), bm, cfg); } catch (const NonFiniteInput& e) {
+      thrown = std::strstr(e.what(), "k") != nullptr;
+    }
+    EXPECT(thrown);
+    thrown = false;
+    try { check_finite({{"q", &q}, {"k", &k}}); } catch (const NonFiniteInput&) { thrown = true; }
+    EXPECT(thrown);
+    // d_out checked by the backward (engine.cpp:196)
+    AttentionOutput f = forward(q, q, q, noop_score(), bm);
+    thrown = false;
+    try { backward(q, q, q, f, k, noop_score(), bm, bm, cfg); } catch (const NonFiniteInput& e) {
+      thrown = std::strstr(e.what(), "d_out") != nullptr;
+    }
+    EXPECT(thrown);
+    AttentionConfig det;
+    det.deterministic = true;
+    DeviceTensor4 dout = random_tensor(13, 1, 2, 256, 128);
+    Gradients g1 = backward(q, q, q, f, dout, noop_score(), bm, bm, det);
+    Gradients g2 = backward(q, q, q, f, dout, noop_score(), bm, bm, det);
+    const auto a1 = to_host_f32(g1.dq), a2 = to_host_f32(g2.dq);
+    EXPECT(std::memcmp(a1.data(), a2.data(), a1.size() * 4) == 0);
+  }
+  // ---- PagedKVCache + convert_mods: paged decode == unpaged, foreign page -> UnmappedPhysicalIndex
+  {
+    const i64 B = 2, H = 2, L = 640, D = 128, ps = 128;
+    PagedKVCache cache(B, B * (L / ps) + B, ps, H, D);
+    cache.shuffle_free_pages(0xFA6E5);
+    DeviceTensor4 kl = random_tensor(31, B, H, L, D), vl = random_tensor(32, B, H, L, D);
+    for (i64 b = 0; b < B; ++b) {
+      DeviceTensor4 kb(1, H, L, D), vb(1, H, L, D);
+      const size_t bytes = static_cast<size_t>(H * L * D * 2);
+      check_cuda(cudaMemcpy(kb.buf.get(), kl.buf.as<char>() + b * bytes, bytes, cudaMemcpyDeviceToDevice), "slice");
+      check_cuda(cudaMemcpy(vb.buf.get(), vl.buf.as<char>() + b * bytes, bytes, cudaMemcpyDeviceToDevice), "slice");
+      cache.assign(b, kb, vb);
+    }
+    EXPECT(cache.seq_len(0) == L && cache.free_pages() == B);
+    DeviceTensor4 q = random_tensor(33, B, H, 1, D);
+    const i64 off = L - 1;
+    BlockMask lbm = create_block_mask(offset_mask(causal(), off), 1, 1, 1, L);
+    BlockMask pbm = convert_block_mask(lbm, cache.table());
+    ConvertedMods cm = convert_mods(causal(), noop_score(), cache.table());
+    AttentionConfig vcfg;
+    vcfg.validate = true;
+    OpCounters ctr;
+    AttentionOutput paged = decode(q, cache, off, cm, pbm, vcfg, &ctr);
+    AttentionOutput unpaged = decode(q, kl, vl, off, causal(), noop_score(), lbm);
+    const auto p1 = to_host_f32(paged.out), u1 = to_host_f32(unpaged.out);
+    EXPECT(std::memcmp(p1.data(), u1.data(), p1.size() * 4) == 0);
+    EXPECT(ctr.score_evals == std::uint64_t(B * H * L));          // every cached token is live
+    EXPECT(ctr.mask_evals == std::uint64_t(B * H * L));           // all tiles partial (q_len 1)
+    // a mask that points batch 1's rows at batch 0's pages: foreign pages
+    fa_block_mask bad = pbm.c;
+    std::vector<int32_t> idx(static_cast<size_t>(B * pbm.c.cols));
+    check_cuda(cudaMemcpy(idx.data(), pbm.c.kv_indices, idx.size() * 4, cudaMemcpyDeviceToHost), "idx");
+    std::vector<int32_t> swapped = idx;
+    for (i64 c = 0; c < pbm.c.cols; ++c) swapped[static_cast<size_t>(pbm.c.cols + c)] = idx[static_cast<size_t>(c)];
+    DeviceBuffer sidx(swapped.size() * 4);
+    check_cuda(cudaMemcpy(sidx.get(), swapped.data(), swapped.size() * 4, cudaMemcpyHostToDevice), "idx");
+    BlockMask pbad = pbm;
+    pbad.c.kv_indices = sidx.as<int32_t>();
+    (void)bad;
+    bool thrown = false;
+    try { decode(q, cache, off, cm, pbad, vcfg); } catch (const UnmappedPhysicalIndex&) { thrown = true; }
+    EXPECT(thrown);
+    thrown = false;
+    try {
+      PagedKVCache small(1, 2, ps, H, D);
+      DeviceTensor4 big(1, H, 3 * ps, D);
+      small.assign(0, big, big);
+    } catch (const OutOfPages&) { thrown = true; }
+    EXPECT(thrown);
+    std::printf("paged decode == unpaged; counters score_evals %llu\n",
+                static_cast<unsigned long long>(ctr.score_evals));
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

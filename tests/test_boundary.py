@@ -60,7 +60,7 @@ def test_status_names():
     lib = _lib.load()
     names = {i: lib.fa_status_name(i).decode() for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 100, 101)}
     assert names[1] == "ShapeMismatch" and names[6] == "BlockMaskMismatch" and names[10] == "UnmappedBlock"
-    assert lib.fa_abi_version() == 2  # v2: fa_mask_desc or_terms / natten / remap
+    assert lib.fa_abi_version() == 3  # v3: flags, counters, phase events, fa_check_finite
 
 
 def test_geometry_validation():
@@ -153,3 +153,115 @@ def test_no_cpu_path():
     with pytest.raises((fa.Unsupported, fa.CudaError, RuntimeError)):
         fa.forward(x, x, x, fa.noop_score(), None or fa.BlockMask(1, 1, 1, 1, 128, 128, 128, 128, x, x, x, x,
                                                                    mask=fa.causal()))
+
+
+def test_forward_unknown_flags():
+    from paper_2412_05496_b200 import _lib
+    lib = _lib.load()
+    a = _fwd_args()
+    a.flags = 0x80
+    assert lib.fa_flex_fwd(C.byref(a), None) == 1
+    assert b"flags" in lib.fa_last_error()
+
+
+def _bwd_args():
+    from paper_2412_05496_b200 import _lib
+    a = _lib.BwdArgs()
+    t = lambda: _tensor(1, 4, 256, 128)  # noqa: E731
+    a.q, a.k, a.v, a.out, a.d_out, a.dq, a.dk, a.dv = t(), t(), t(), t(), t(), t(), t(), t()
+    a.lse = 0x2000
+    bm = _lib.BlockMaskC()
+    bm.b_dims = bm.h_dims = 1
+    bm.rows = bm.cols = 2
+    bm.bs_q = bm.bs_kv = 128
+    bm.q_len = bm.kv_len = 256
+    for f in ("kv_num_blocks", "kv_indices", "full_kv_num_blocks", "full_kv_indices", "q_num_blocks",
+              "q_indices", "full_q_num_blocks", "full_q_indices"):
+        setattr(bm, f, 0x3000)
+    a._bm = bm
+    a.bm = C.pointer(bm)
+    a.gqa_group = 1
+    a.workspace = 0x4000
+    a.workspace_bytes = 1 << 30
+    return a
+
+
+@pytest.mark.parametrize("mutate,status", [
+    (lambda a: setattr(a, "dq", _tensor(1, 4, 128, 128)), 1),           # dq must match q
+    (lambda a: setattr(a, "dk", _tensor(1, 4, 256, 64)), 1),            # dk must match k
+    (lambda a: setattr(a, "dv", _tensor(1, 4, 256, 128, dtype=0)), 1),  # dtype of dv
+    (lambda a: setattr(a, "d_out", _tensor(1, 4, 256, 128, dtype=0)), 1),
+    (lambda a: setattr(a, "out", _tensor(1, 4, 255, 128)), 7),          # StaleStatistics
+    (lambda a: setattr(a._bm, "q_indices", None), 6),                    # q side required
+    (lambda a: setattr(a, "workspace_bytes", 16), 1),
+    (lambda a: setattr(a, "flags", 0x40), 1),
+])
+def test_backward_validation_errors(mutate, status):
+    from paper_2412_05496_b200 import _lib
+    lib = _lib.load()
+    a = _bwd_args()
+    mutate(a)
+    assert lib.fa_flex_bwd(C.byref(a), None) == status
+    assert lib.fa_last_error()
+
+
+def _decode_args(paged=False):
+    from paper_2412_05496_b200 import _lib
+    a = _lib.DecodeArgs()
+    a.q, a.out = _tensor(2, 4, 1, 128), _tensor(2, 4, 1, 128)
+    a.k_cache = a.v_cache = _tensor(1 if paged else 2, 4, 1024, 128)
+    a.lse = 0x2000
+    bm = _lib.BlockMaskC()
+    bm.b_dims, bm.h_dims, bm.rows, bm.cols = (2 if paged else 1), 1, 1, 8
+    bm.bs_q = bm.bs_kv = 128
+    bm.q_len, bm.kv_len = 1, 1024
+    bm.kv_num_blocks = bm.kv_indices = bm.full_kv_num_blocks = bm.full_kv_indices = 0x3000
+    a._bm = bm
+    a.bm = C.pointer(bm)
+    if paged:
+        pt = _lib.PageTableC()
+        pt.batches, pt.max_logical_pages, pt.num_physical_pages, pt.page_size = 2, 8, 8, 128
+        pt.table = pt.phys_to_logical = pt.owner = pt.seq_len = 0x5000
+        a._pt = pt
+        a.pt = C.pointer(pt)
+    a.offset = 1023
+    a.gqa_group = 1
+    a.workspace = 0x4000
+    a.workspace_bytes = 1 << 30
+    return a
+
+
+@pytest.mark.parametrize("paged", [False, True])
+@pytest.mark.parametrize("mutate,status", [
+    (lambda a: setattr(a, "bm", None), 6),                              # NULL mask checked first
+    (lambda a: setattr(a, "out", _tensor(2, 4, 2, 128)), 1),            # out must match q
+    (lambda a: setattr(a, "out", _tensor(2, 4, 1, 128, dtype=0)), 1),
+    (lambda a: setattr(a, "offset", 1024), 8),                          # OffsetOutOfRange
+    (lambda a: (setattr(a.mask, "remap", 0x10), setattr(a.mask, "remap_len", 512)), 3),  # kv range
+    (lambda a: (setattr(a.mask, "terms", 4), setattr(a.mask, "doc_ids", 0x10),
+                setattr(a.mask, "doc_len", 1000)), 3),
+    (lambda a: setattr(a._bm, "h_dims", 3), 6),
+])
+def test_decode_validation_errors(paged, mutate, status):
+    from paper_2412_05496_b200 import _lib
+    lib = _lib.load()
+    a = _decode_args(paged)
+    mutate(a)
+    assert lib.fa_flex_decode(C.byref(a), None) == status, lib.fa_last_error()
+    assert lib.fa_last_error()
+
+
+def test_paged_decode_mask_range_uses_max_seq_len():
+    # the mask is evaluated only below the sequences' lengths: a table spanning max_seq_len is
+    # enough even when the page table has room for more logical pages
+    from paper_2412_05496_b200 import _lib
+    lib = _lib.load()
+    a = _decode_args(paged=True)
+    a.offset = 299
+    a.mask.remap, a.mask.remap_len = 0x10, 300
+    a._pt.max_seq_len = 300
+    a.flags = 0x80  # stop right after argument validation (unknown flag)
+    assert lib.fa_flex_decode(C.byref(a), None) == 1
+    assert b"flags" in lib.fa_last_error()
+    a._pt.max_seq_len = 0  # unknown: the whole logical page range must be covered
+    assert lib.fa_flex_decode(C.byref(a), None) == 3

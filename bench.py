@@ -42,6 +42,9 @@ CONFIGS = {
                B=2, Hq=32, Hkv=8, L=8192, D=128, mask="causal", score="softcap",
                fwd_gflop=1099.65, live_per_bh=33558528),
 }
+# C5 (decode, HBM-bound): Q_LEN 1, paged KV (page 128) via the converted BlockMask
+C5 = dict(desc="paged decode Q_LEN=1 B64 H32 KV_LEN 32768 page 128 D128 bf16, offset_mask(causal, 32767)",
+          B=64, H=32, L=32768, D=128, ps=128)
 DOC_LENGTHS = [1004, 350, 639, 2533, 190, 1601, 7058, 3009]
 SEED = 0x5EED0001  # per-config seed S_c (bench.cpp:414); Q/K/V/dO = S_c+1..+4
 
@@ -63,13 +66,14 @@ def peaks():
         return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes/launch of the dominant kernel from the committed ncu summary, else None."""
+def profile_traffic(key):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of one kernel from
+    the committed ncu --set full summary of this build (profiles/ncu_summary.json), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("bwd_dram_bytes_per_launch")
+        return d["kernels"][key]["dram_bytes"]
     except Exception:
         return None
 
@@ -189,6 +193,134 @@ def cpu_reference_sample(c, kind_pref="reference"):
     return dict(seconds=t2 - t0, fwd_s=t1 - t0, bwd_s=t2 - t1, cores=1, kind="port", gflop=slice_gflop)
 
 
+def timed_events(n):
+    import torch
+    return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+
+
+def inputs_for(fa, c, seed, dev):
+    B, Hq, Hkv, L, D = c["B"], c["Hq"], c["Hkv"], c["L"], c["D"]
+    q = fa.random_tensor(seed + 1, (B, Hq, L, D), device=dev)
+    k = fa.random_tensor(seed + 2, (B, Hkv, L, D), device=dev)
+    v = fa.random_tensor(seed + 3, (B, Hkv, L, D), device=dev)
+    do = fa.random_tensor(seed + 4, (B, Hq, L, D), device=dev)
+    return q, k, v, do
+
+
+def measure_builder(fa, mask, L, dev, reps=20):
+    """create_block_mask (+ transpose) device time, mask evaluations/s and output GB/s."""
+    import torch
+    for _ in range(3):
+        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / reps * 1000.0
+    R = C_ = -(-L // 128)
+    out_bytes = 2 * (2 * R * C_ + R + C_) * 4  # 8 int32 arrays (SURVEY §8d builder bytes)
+    if mask.doc_ids is not None:
+        out_bytes += mask.doc_ids.numel() * 4
+    return bm, {"us": round(us, 2), "evals_per_s": float(f"{L * L / (us * 1e-6):.4g}"),
+                "gb_per_s": round(out_bytes / (us * 1e-6) / 1e9, 3), "bytes": out_bytes}
+
+
+def measure_attention(fa, name, c, dev, steps, warmup, seed, stream):
+    """fwd + bwd of one config: step time, per-phase and per-kernel device times (CUDA events on
+    the launching stream; the backward records events around its preprocess / main / convert)."""
+    import torch
+    q, k, v, do = inputs_for(fa, c, seed, dev)
+    mask, score = build_mods(fa, c, dev)
+    cfg = fa.AttentionConfig(gqa_group=c["Hq"] // c["Hkv"])
+    bm, builder = measure_builder(fa, mask, c["L"], dev)
+    fwd_ev, bwd_ev, ph = timed_events(steps), timed_events(steps), [timed_events(1)[0] + timed_events(1)[0]
+                                                                    for _ in range(steps)]
+
+    def step(i=None):
+        if i is not None:
+            fwd_ev[i][0].record(stream)
+        res = fa.forward(q, k, v, score, bm, cfg)
+        if i is not None:
+            fwd_ev[i][1].record(stream)
+            bwd_ev[i][0].record(stream)
+        g = fa.backward(q, k, v, res, do, score, bm, cfg=cfg, phase_events=ph[i] if i is not None else None)
+        if i is not None:
+            bwd_ev[i][1].record(stream)
+        return res, g
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+    bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bwd_ev)
+    pre_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ph)
+    main_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ph)
+    conv_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in ph)
+    del q, k, v, do
+    fg = c["fwd_gflop"]
+    return {"workload": f"{name}: {c['desc']}", "ms_per_step": round(ms, 4),
+            "fwd_bwd_tflops": round(3.5 * fg / ms, 2), "fwd_ms": round(fwd_ms, 4),
+            "fwd_tflops": round(fg / fwd_ms, 2), "bwd_ms": round(bwd_ms, 4),
+            "bwd_tflops": round(2.5 * fg / bwd_ms, 2),
+            "bwd_kernels_ms": {"preprocess": round(pre_ms, 4), "main": round(main_ms, 4),
+                               "dq_convert": round(conv_ms, 4)},
+            "bwd_main_tflops": round(2.5 * fg / main_ms, 2),
+            "fwd_gflop": fg, "block_mask": builder}
+
+
+def measure_decode(fa, dev, steps, warmup, stream, hbm):
+    """C5: paged split-KV decode, HBM-bound (bytes = K + V of every visited page)."""
+    import torch
+    c = C5
+    B, H, L, D, ps = c["B"], c["H"], c["L"], c["D"], c["ps"]
+    pages = B * (L // ps) + B
+    cache = fa.PagedKVCache(B, pages, ps, H, D, device=dev)
+    cache.shuffle_free_pages(SEED ^ 0xFA6E5)
+    for b in range(B):  # logical K/V generated per batch element and scattered into pages
+        kb = fa.random_tensor(SEED + 2, (1, H, L, D), device=dev, first=b * H * L * D)
+        vb = fa.random_tensor(SEED + 3, (1, H, L, D), device=dev, first=b * H * L * D)
+        cache.assign(b, kb, vb)
+    del kb, vb
+    q = fa.random_tensor(SEED + 1, (B, H, 1, D), device=dev)
+    off = L - 1
+    lbm = fa.create_block_mask(fa.offset_mask(fa.causal(), off), 1, 1, 1, L, device=dev)
+    pt = cache.page_table()
+    pbm = fa.convert_block_mask(lbm, pt)
+    kp, vp = cache.k_phys(), cache.v_phys()
+
+    def call():
+        return fa.decode(q, kp, vp, off, fa.causal(), fa.noop_score(), pbm, page_table=pt)
+
+    for _ in range(warmup):
+        call()
+    torch.cuda.synchronize()
+    ev = timed_events(steps)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        call()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    kv_bytes = 2 * B * H * L * D * 2
+    other = B * H * D * 2 * 2 + B * H * 4 + pbm.kv_indices.numel() * 4 * 2
+    gbs = (kv_bytes + other) / (ms * 1e-3) / 1e9
+    del cache, kp, vp
+    return {"workload": f"C5: {c['desc']}", "ms_per_step": round(ms, 4), "gb_per_s": round(gbs, 1),
+            "hbm_frac": round(gbs / hbm, 4), "bytes_per_step": kv_bytes + other,
+            "gflop": round(4 * B * H * L * D / 1e9, 2),
+            "l2": "34.4 GB of K/V per step >> 126 MB L2 (no flush needed)"}
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -198,32 +330,38 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     import paper_2412_05496_b200 as fa
+    from paper_2412_05496_b200 import shard
 
     c = CONFIGS[args.config]
     B, Hq, Hkv, L, D = c["B"], c["Hq"], c["Hkv"], c["L"], c["D"]
     mask, score = build_mods(fa, c, dev)
-    seed = SEED + 1000003 * rank  # each rank: its own batch of the sharded job
-    q = fa.random_tensor(seed + 1, (B, Hq, L, D), device=dev)
-    k = fa.random_tensor(seed + 2, (B, Hkv, L, D), device=dev)
-    v = fa.random_tensor(seed + 3, (B, Hkv, L, D), device=dev)
-    do = fa.random_tensor(seed + 4, (B, Hq, L, D), device=dev)
     cfg = fa.AttentionConfig(gqa_group=Hq // Hkv)
-
-    # BlockMask build (timed separately; HBM-tiny, mask-evaluation bound)
-    for _ in range(3):
-        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10):
-        bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
-    e1.record()
-    torch.cuda.synchronize()
-    mask_us = e0.elapsed_time(e1) / 10 * 1000.0
+    if args.strong and world > 1:
+        # strong scaling: ONE job of the config; this rank owns a contiguous range of its
+        # (batch, kv head) units with all G q heads of each (engine.cpp:311-331), no collective
+        G = Hq // Hkv
+        sh = shard.rect_shard(B, Hkv, world, rank)
+        q, k, v, do = shard.slice_job(*inputs_for(fa, c, SEED, dev), G, sh)
+        score = shard.shard_score(score, G, sh)
+        my_frac = (sh[1] - sh[0]) * (sh[3] - sh[2]) / (B * Hkv)
+        torch.cuda.empty_cache()
+        job_gflop = 3.5 * c["fwd_gflop"]
+        scaling = "strong"
+        parallelism = (f"dp{world}: one {args.config} job split into {world} rectangles of its {B * Hkv} "
+                       f"(batch, kv-head) units, no collective")
+    else:
+        seed = SEED + 1000003 * rank  # each rank: its own batch of the sharded job
+        q, k, v, do = inputs_for(fa, c, seed, dev)
+        job_gflop = 3.5 * c["fwd_gflop"] * world
+        my_frac = 1.0
+        scaling = "weak"
+        parallelism = f"dp{world}: one (b,h)-shard per GPU, no collective"
+    bm = fa.create_block_mask(mask, 1, 1, L, L, device=dev)
 
     stream = torch.cuda.current_stream()
-    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    bwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    steps = args.steps
+    fwd_ev, bwd_ev = timed_events(steps), timed_events(steps)
+    ph = [timed_events(1)[0] + timed_events(1)[0] for _ in range(steps)]
 
     def step(i=None):
         if i is not None:
@@ -232,7 +370,7 @@ def run_ours(args):
         if i is not None:
             fwd_ev[i][1].record(stream)
             bwd_ev[i][0].record(stream)
-        g = fa.backward(q, k, v, res, do, score, bm, cfg=cfg)
+        g = fa.backward(q, k, v, res, do, score, bm, cfg=cfg, phase_events=ph[i] if i is not None else None)
         if i is not None:
             bwd_ev[i][1].record(stream)
         return res, g
@@ -253,7 +391,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        for i in range(args.steps):
+        for i in range(steps):
             step(i)
         t_end.record(stream)
         torch.cuda.synchronize()
@@ -262,11 +400,12 @@ def run_ours(args):
     ms = t_start.elapsed_time(t_end)
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
     bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in bwd_ev)
+    main_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ph)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms, fwd_ms, bwd_ms], device=dev)
+        t = torch.tensor([ms, fwd_ms, bwd_ms, main_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, fwd_ms, bwd_ms = t.tolist()
+        ms, fwd_ms, bwd_ms, main_ms = t.tolist()
 
     # ---- e2e: same step through the public API with host buffers, H2D + D2H inside ----
     # Every step copies its four inputs host->device and its five results device->host (pinned
@@ -276,9 +415,9 @@ def run_ours(args):
     for h_, d_ in zip(host, (q, k, v, do)):
         h_.copy_(d_)
     outs = [[torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (q, q, k, v)] for _ in range(2)]
-    lse_h = [torch.empty((B, Hq, L), dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    lse_h = [torch.empty(q.shape[:3], dtype=torch.float32, pin_memory=True) for _ in range(2)]
     dbuf = [[torch.empty_like(x) for x in (q, k, v, do)] for _ in range(2)]
-    e2e_steps = max(2, min(args.steps, 8))
+    e2e_steps = max(2, min(steps, 8))
     s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
     def e2e_run(nsteps):
@@ -332,6 +471,23 @@ def run_ours(args):
         barrier()
     h2d = sum(x.numel() * x.element_size() for x in host)
     d2h = sum(x.numel() * x.element_size() for x in outs[0]) + lse_h[0].numel() * 4
+    del host, outs, lse_h, dbuf, q, k, v, do
+    torch.cuda.empty_cache()
+
+    peak, hbm, peak_kind = peaks()
+    # ---- every other BASELINE workload, one GPU (rank 0 of a single-process run) ----
+    per_config = {}
+    if world == 1 and not args.headline_only:
+        for name in ("C2", "C3", "C4"):
+            per_config[name] = measure_attention(fa, name, CONFIGS[name], dev, max(5, min(steps, 20)),
+                                                 max(3, args.warmup), SEED, stream)
+            per_config[name]["pct_of_peak_fwd_bwd"] = round(100 * per_config[name]["fwd_bwd_tflops"] / peak, 2)
+            torch.cuda.empty_cache()
+        try:
+            per_config["C5"] = measure_decode(fa, dev, max(5, min(steps, 20)), max(3, args.warmup), stream, hbm)
+        except Exception as e:  # reported, not fatal
+            per_config["C5"] = {"error": str(e)[:200]}
+        torch.cuda.empty_cache()
 
     if rank != 0:
         if world > 1:
@@ -339,38 +495,38 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    peak, hbm, peak_kind = peaks()
-    step_gflop = 3.5 * c["fwd_gflop"] * world
-    ms_per_step = ms / args.steps
-    tflops = step_gflop / ms_per_step
+    ms_per_step = ms / steps
+    tflops = job_gflop / ms_per_step
     bwd_gflop = 2.5 * c["fwd_gflop"]
-    achieved = bwd_gflop / bwd_ms  # TFLOP/s of the dominant kernel (backward), per GPU
+    achieved = bwd_gflop * my_frac / main_ms  # the dominant kernel alone, this GPU
     line = {
-        "metric": "effective TFLOPS (unmasked FLOPs) fwd+bwd, C2 sliding_window(1024)+ALiBi",
-        "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "metric": f"effective TFLOPS (unmasked FLOPs) fwd+bwd, {args.config} "
+                  f"{'sliding_window(1024)+ALiBi' if args.config == 'C2' else c['desc']}",
+        "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: SplitMix64 uniform[-1,1) (random.hpp) generated on device, bf16 RNE",
-        "config": {"workload": f"{args.config}: {c['desc']}", "global_batch": B * world, "seq_len": L,
-                   "heads_q": Hq, "heads_kv": Hkv, "head_dim": D,
-                   "parallelism": f"dp{world}: one (b,h)-shard per GPU, no collective",
+        "config": {"workload": f"{args.config}: {c['desc']}", "global_batch": B * (world if scaling == "weak" else 1),
+                   "seq_len": L, "heads_q": Hq, "heads_kv": Hkv, "head_dim": D, "parallelism": parallelism,
                    "l2": "inputs 4 x 134 MB > 126 MB L2 (no flush needed)",
                    "block_mask": "built once outside the timed region (builder timed separately)"},
-        "fwd_tflops": round(c["fwd_gflop"] / fwd_ms, 2), "bwd_tflops": round(bwd_gflop / bwd_ms, 2),
+        "fwd_tflops": round(c["fwd_gflop"] * my_frac / fwd_ms, 2), "bwd_tflops": round(bwd_gflop * my_frac / bwd_ms, 2),
         "fwd_ms": round(fwd_ms, 4), "bwd_ms": round(bwd_ms, 4),
         "pct_of_peak": round(100.0 * tflops / world / peak, 2), "peak_tflops": peak, "peak_kind": peak_kind,
-        "block_mask_us": round(mask_us, 2),
-        "roofline": {"bound": "tensor", "kernel": "flex_bwd_sm100 (+preprocess/convert)",
+        "roofline": {"bound": "tensor", "kernel": "flex_bwd_sm100_kernel (backward main kernel alone)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": profile_traffic(),
-                     "algorithmic_per_launch": f"{bwd_gflop:.2f} GFLOP = 2.5 x 4*D*N_live"},
-        "e2e": {"value": round(step_gflop / e2e_ms, 2), "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": profile_traffic(f"{args.config}_bwd_main"),
+                     "kernel_ms": round(main_ms, 4),
+                     "algorithmic_per_launch": f"{bwd_gflop * my_frac:.2f} GFLOP = 2.5 x 4*D*N_live"},
+        "e2e": {"value": round(job_gflop / e2e_ms, 2), "unit": "TFLOP/s",
                 "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                 "ms_per_step": round(e2e_ms, 3),
                 "note": f"{e2e_steps} steps pipelined over H2D / compute / D2H streams"},
         "gpu_launches": int(launches),
         "clocks": sampler.summary(),
     }
+    if per_config:
+        line["configs"] = per_config
     if world == 1 and not args.no_cpu_baseline:
         try:
             cb = cpu_reference_sample(c)
@@ -426,6 +582,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--headline-only", action="store_true", help="skip the per-config C2-C5 measurements")
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: split ONE job's (batch, kv-head) units across the ranks (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -1,16 +1,17 @@
 // block_mask.cu — BlockMask construction on sm_100a.
 //
 // Replaces create_block_mask (block_mask.cpp:79-115), transpose (:161-178) and
-// convert_block_mask (paged_kv.cpp:154-228). Two kernels:
-//   1. classify: one warp per (b, h, r, c) tile evaluates mask_mod over the
-//      tile's in-range positions, 32 kv positions per step, and decides
-//      EMPTY / PARTIAL / FULL with __any_sync/__all_sync, leaving early as soon
-//      as the tile is provably mixed (the reference's early exit, :96-105).
-//      Ragged tiles are never FULL (:91-94). Output: one byte per tile.
-//   2. compact: one warp per kv-side row and per q-side column turns the byte
-//      grid into ascending compacted index lists with ballot + popc prefix
-//      sums, counts, and zero-filled tails (:50-52), i.e. the kv_num_blocks /
-//      kv_indices / full_kv_* arrays and the transposed q-side arrays.
+// convert_block_mask (paged_kv.cpp:154-228). Two kernels per build:
+//   1. classify: one warp per (b, h, r, c) tile. The mask functor first tries a closed form
+//      over the whole tile (MaskFn::tile_class: causal / sliding-window / prefix ranges,
+//      document-id ranges of the tile's rows and columns, neighbourhood distances, composed
+//      with AND = min / OR = max); only tiles it cannot decide are evaluated, lanes over query
+//      rows and mask_mod 32 kv positions per word (MaskFn::bits32), leaving early as soon as
+//      the tile is provably mixed (the reference's early exit, :96-105). Ragged tiles are
+//      never FULL (:91-94). Output: one byte per tile.
+//   2. compact: one warp per kv-side row and per q-side column (one launch) turns the byte
+//      grid into ascending compacted index lists with ballot + popc prefix sums, counts and
+//      zero-filled tails (:50-52): kv_num_blocks / kv_indices / full_kv_* and the q side.
 // All integer work; HBM traffic is the grid plus the int32 outputs.
 #include <cuda_runtime.h>
 
@@ -41,17 +42,31 @@ __global__ void __launch_bounds__(256) classify_kernel(MaskT mask, int b_dims, i
     const int q0 = r * bs_q, q1 = min(q0 + bs_q, q_len);
     const int k0 = c * bs_kv, k1 = min(k0 + bs_kv, kv_len);
     const bool ragged = (q1 - q0 != bs_q) || (k1 - k0 != bs_kv);
-    bool any = false, all = true;
-    for (int q = q0; q < q1 && !(any && !all); ++q) {
-      for (int kb = k0; kb < k1; kb += 32) {
-        const int kv = kb + lane;
-        const bool in = kv < k1;
-        const bool v = in && mask(b, h, q, kv);
-        any = any || __any_sync(0xffffffffu, v);
-        all = all && __all_sync(0xffffffffu, v || !in);
+    // closed form first (causal / sliding / prefix ranges, document id ranges, ...)
+    const int cls = mask.tile_class(b, h, q0, q1, k0, k1, lane);
+    bool any = cls == kTileAll, all = cls == kTileAll;
+    if (cls == kTileMixed) {
+      // evaluate: lanes take query rows, mask_mod 32 kv positions per word (bits32); stop as
+      // soon as the tile is provably mixed (the reference's early exit, block_mask.cpp:96-105)
+      any = false;
+      all = true;
+      for (int qb = q0; qb < q1; qb += 32) {
+        const int q = qb + lane;
+        bool my_any = false, my_all = true;
+        if (q < q1) {
+          for (int kw = k0; kw < k1; kw += 32) {
+            const uint32_t valid = range_bits32(kw, kw, k1 - 1);
+            const uint32_t bits = mask.bits32(b, h, q, kw, k1) & valid;
+            my_any |= bits != 0u;
+            my_all &= bits == valid;
+          }
+        }
+        any = __any_sync(0xffffffffu, my_any) || any;
+        all = __all_sync(0xffffffffu, my_all) && all;
         if (any && !all) break;
       }
     }
+    // ragged tiles are never FULL (block_mask.cpp:91-94)
     if (lane == 0) grid[tile] = !any ? kEmpty : ((all && !ragged) ? kFull : kPartial);
   }
 }
@@ -90,6 +105,48 @@ __global__ void __launch_bounds__(256) compact_kernel(const uint8_t* __restrict_
     if (lane == 0) {
       part_num[line] = np;
       full_num[line] = nf;
+    }
+  }
+}
+
+// Both sides in one launch: warps [0, nrows) compact kv-side rows, the rest q-side columns.
+__global__ void __launch_bounds__(256) compact_both_kernel(const uint8_t* __restrict__ grid, int bh, int rows,
+                                                           int cols, int32_t* __restrict__ kpn,
+                                                           int32_t* __restrict__ kpi, int32_t* __restrict__ kfn,
+                                                           int32_t* __restrict__ kfi, int32_t* __restrict__ qpn,
+                                                           int32_t* __restrict__ qpi, int32_t* __restrict__ qfn,
+                                                           int32_t* __restrict__ qfi) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nrows = bh * rows, nlines = nrows + (qpn != nullptr ? bh * cols : 0);
+  for (int line = warp_global; line < nlines; line += nwarps) {
+    const bool kv_side = line < nrows;
+    const int li = kv_side ? line : line - nrows;
+    const int per = kv_side ? rows : cols;            // lines per (b, h)
+    const int len = kv_side ? cols : rows;            // elements per line
+    const int bhi = li / per, l = li % per;
+    const long long base = static_cast<long long>(bhi) * rows * cols + (kv_side ? static_cast<long long>(l) * cols : l);
+    const int estride = kv_side ? 1 : cols;
+    int32_t* pi = (kv_side ? kpi : qpi) + static_cast<long long>(li) * len;
+    int32_t* fi = (kv_side ? kfi : qfi) + static_cast<long long>(li) * len;
+    int np = 0, nf = 0;
+    for (int j0 = 0; j0 < len; j0 += 32) {
+      const int j = j0 + lane;
+      const uint8_t kind = j < len ? grid[base + static_cast<long long>(j) * estride] : kEmpty;
+      const unsigned pm = __ballot_sync(0xffffffffu, kind == kPartial);
+      const unsigned fm = __ballot_sync(0xffffffffu, kind == kFull);
+      const unsigned lower = (1u << lane) - 1u;
+      if (kind == kPartial) pi[np + __popc(pm & lower)] = j;   // push_block :65-66
+      if (kind == kFull) fi[nf + __popc(fm & lower)] = j;      // push_block :62-64
+      np += __popc(pm);
+      nf += __popc(fm);
+    }
+    for (int j = np + lane; j < len; j += 32) pi[j] = 0;        // zero tails, make_empty :50-52
+    for (int j = nf + lane; j < len; j += 32) fi[j] = 0;
+    if (lane == 0) {
+      (kv_side ? kpn : qpn)[li] = np;
+      (kv_side ? kfn : qfn)[li] = nf;
     }
   }
 }
@@ -167,20 +224,12 @@ static void launch_classify(MaskT m, int bd, int hd, int rows, int cols, int ql,
 
 static fa_status compact_both(int bd, int hd, int rows, int cols, const uint8_t* grid,
                               fa_block_mask* bm, cudaStream_t st) {
-  // kv side: line = (b,h,r), elements c contiguous
-  const int nrows = bd * hd * rows;
-  compact_kernel<<<grid_for(nrows), 256, 0, st>>>(grid, nrows, cols, rows, rows * cols, cols, 1,
-                                                  bm->kv_num_blocks, bm->kv_indices,
-                                                  bm->full_kv_num_blocks, bm->full_kv_indices);
+  const long long lines = static_cast<long long>(bd) * hd * (rows + (bm->q_num_blocks != nullptr ? cols : 0));
+  compact_both_kernel<<<grid_for(lines), 256, 0, st>>>(grid, bd * hd, rows, cols, bm->kv_num_blocks,
+                                                       bm->kv_indices, bm->full_kv_num_blocks,
+                                                       bm->full_kv_indices, bm->q_num_blocks, bm->q_indices,
+                                                       bm->full_q_num_blocks, bm->full_q_indices);
   count_launch();
-  if (bm->q_num_blocks != nullptr) {
-    // q side: line = (b,h,c), elements r strided by cols
-    const int ncols = bd * hd * cols;
-    compact_kernel<<<grid_for(ncols), 256, 0, st>>>(grid, ncols, rows, cols, rows * cols, 1, cols,
-                                                    bm->q_num_blocks, bm->q_indices,
-                                                    bm->full_q_num_blocks, bm->full_q_indices);
-    count_launch();
-  }
   FA_CHECK_CUDA(cudaGetLastError());
   return FA_OK;
 }

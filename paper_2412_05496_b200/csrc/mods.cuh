@@ -109,9 +109,96 @@ __device__ __forceinline__ uint32_t doc_match_bits32(const int32_t* ids, int len
   return bits;
 }
 
+// Tile classes of a mask term over a whole tile (the BlockMask builder's closed forms):
+// the AND of terms is the min, the OR of groups the max.
+enum : int { kTileNone = 0, kTileMixed = 1, kTileAll = 2 };
+// q in [a0, a1], kv in [c0, c1] (inclusive, offsets applied)
+__device__ __forceinline__ int tile_causal(int a0, int a1, int c0, int c1) {
+  if (a0 >= c1) return kTileAll;
+  if (a1 < c0) return kTileNone;
+  return kTileMixed;
+}
+__device__ __forceinline__ int tile_sliding(int a0, int a1, int c0, int c1, int w) {
+  if (a1 < c0 || a0 - c1 > w) return kTileNone;  // no q >= kv, or every q - kv > w
+  if (a0 >= c1 && a1 - c0 <= w) return kTileAll;
+  return kTileMixed;
+}
+__device__ __forceinline__ int tile_prefix(int a0, int a1, int c0, int c1, int prefix) {
+  if (c1 < prefix || a0 >= c1) return kTileAll;
+  if (c0 >= prefix && a1 < c0) return kTileNone;
+  return kTileMixed;
+}
+// document ids over q in [a0, a1] and kv in [c0, c1]: all equal -> all; disjoint id ranges ->
+// none (warp-collective: every lane passes the same arguments)
+__device__ __forceinline__ int tile_document(const int32_t* ids, int a0, int a1, int c0, int c1, int lane) {
+  int qmin = INT_MAX, qmax = INT_MIN, kmin = INT_MAX, kmax = INT_MIN;
+  for (int i = a0 + lane; i <= a1; i += 32) {
+    const int d = __ldg(ids + i);
+    qmin = min(qmin, d);
+    qmax = max(qmax, d);
+  }
+  for (int i = c0 + lane; i <= c1; i += 32) {
+    const int d = __ldg(ids + i);
+    kmin = min(kmin, d);
+    kmax = max(kmax, d);
+  }
+  qmin = __reduce_min_sync(0xffffffffu, qmin);
+  qmax = __reduce_max_sync(0xffffffffu, qmax);
+  kmin = __reduce_min_sync(0xffffffffu, kmin);
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (qmax < kmin || kmax < qmin) return kTileNone;
+  if (qmin == qmax && kmin == kmax && qmin == kmin) return kTileAll;
+  return kTileMixed;
+}
+// na_naive: no pair within the radius when the canvas rows (or, for single-row ranges, the
+// columns) are farther apart than the radius
+__device__ __forceinline__ int tile_natten(int a0, int a1, int c0, int c1, int w, int rad) {
+  const int rq0 = a0 / w, rq1 = a1 / w, rk0 = c0 / w, rk1 = c1 / w;
+  if (max(0, max(rq0 - rk1, rk0 - rq1)) > rad) return kTileNone;
+  if (rq0 == rq1 && rk0 == rk1) {
+    const int cq0 = a0 % w, cq1 = a1 % w, ck0 = c0 % w, ck1 = c1 % w;
+    if (max(0, max(cq0 - ck1, ck0 - cq1)) > rad) return kTileNone;
+  }
+  return kTileMixed;
+}
+
 template <int K>
 struct MaskFn {
   MaskParams p;
+  // Class of the tile q in [q0, q1), kv in [k0, k1) (non-empty, in bounds): kTileAll /
+  // kTileNone when decidable in closed form, else kTileMixed (the builder then evaluates it).
+  // Warp-collective (every lane passes the same tile).
+  __device__ __forceinline__ int tile_class(int b, int h, int q0, int q1, int k0, int k1, int lane) const {
+    (void)b; (void)h;
+    const int a0 = q0 + p.q_offset, a1 = q1 - 1 + p.q_offset, c0 = k0, c1 = k1 - 1;
+    if constexpr (K == kMaskNoop) {
+      return kTileAll;
+    } else if constexpr (K == kMaskCausalOnly) {
+      return tile_causal(a0, a1, c0, c1);
+    } else if constexpr (K == kMaskSlidingOnly) {
+      return tile_sliding(a0, a1, c0, c1, p.window);
+    } else if constexpr (K == kMaskDocCausal) {
+      const int c = tile_causal(a0, a1, c0, c1);
+      if (c == kTileNone) return c;
+      return min(c, tile_document(p.doc_ids, a0, a1, c0, c1, lane));
+    } else {
+      if (p.remap != nullptr) return kTileMixed;
+      int g = group_class(p.terms, a0, a1, c0, c1, lane);
+      if (p.or_terms != 0u && g != kTileAll) g = max(g, group_class(p.or_terms, a0, a1, c0, c1, lane));
+      return g;
+    }
+  }
+  __device__ __forceinline__ int group_class(uint32_t t, int a0, int a1, int c0, int c1, int lane) const {
+    if (t & kMaskNever) return kTileNone;
+    int c = kTileAll;
+    if (t & kMaskCausal) c = min(c, tile_causal(a0, a1, c0, c1));
+    if (t & kMaskSliding) c = min(c, tile_sliding(a0, a1, c0, c1, p.window));
+    if (t & kMaskPrefix) c = min(c, tile_prefix(a0, a1, c0, c1, p.prefix));
+    if (t & kMaskNatten) c = min(c, tile_natten(a0, a1, c0, c1, p.na_w, p.na_radius));
+    if (t & kMaskHash) c = min(c, p.hash_density <= 0 ? kTileNone : (p.hash_density >= 256 ? kTileAll : kTileMixed));
+    if ((t & kMaskDocument) && c != kTileNone) c = min(c, tile_document(p.doc_ids, a0, a1, c0, c1, lane));
+    return c;
+  }
   // kv positions >= kv_lim are reported as 0 (bounds of bound_mask, block_mask.cpp:14-19)
   __device__ __forceinline__ uint32_t bits32(int b, int h, int q, int kv0, int kv_lim) const {
     const int qq = q + p.q_offset;

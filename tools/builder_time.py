@@ -26,11 +26,18 @@ for name, m, L in cases:
     for _ in range(3):
         fa.create_block_mask(m, 1, 1, ql, kl, device=dev)
     torch.cuda.synchronize()
+    n = 20
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            keep = [fa.create_block_mask(m, 1, 1, ql, kl, device=dev) for _ in range(n)]
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    n = 20
-    for _ in range(n):
-        fa.create_block_mask(m, 1, 1, ql, kl, device=dev)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / n * 1000

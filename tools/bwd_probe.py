@@ -1,6 +1,6 @@
-"""Backward diagnostics at a BASELINE config: device time, the per-phase cycle trace of CTA 0
-(FA_BWD_TRACE) and the time with the dQ reductions switched off (FA_BWD_EXP=1, wrong results —
-diagnosis only). Usage: python tools/bwd_probe.py [C2|C3|C4 ...]"""
+"""Backward diagnostics at a BASELINE config: device time and, with the instrumented build
+(make trace + FA_LIB_PATH), the per-phase cycle trace of CTA 0 (FA_BWD_TRACE).
+Usage: python tools/bwd_probe.py [C2|C3|C4 ...]"""
 import os
 import sys
 
@@ -27,11 +27,8 @@ def main(names):
         cfg = fa.AttentionConfig(gqa_group=c["Hq"] // c["Hkv"])
         res = fa.forward(q, k, v, c["score"], bm, cfg)
         run = lambda: fa.backward(q, k, v, res, do, c["score"], bm, cfg=cfg)  # noqa: E731
-        for exp in ("0", "1"):
-            os.environ["FA_BWD_EXP"] = exp
-            t = timeit(run, iters=5, warm=2)
-            print(f"{name} bwd exp={exp} {t:.3f} ms  {2.5 * c['gf'] / t:.1f} TFLOPS", flush=True)
-        os.environ["FA_BWD_EXP"] = os.environ.get("TRACE_EXP", "0")
+        t = timeit(run, iters=5, warm=2)
+        print(f"{name} bwd exp=0 {t:.3f} ms  {2.5 * c['gf'] / t:.1f} TFLOPS", flush=True)
         os.environ["FA_BWD_TRACE"] = os.environ.get("TRACE_LEVEL", "1")
         run()
         torch.cuda.synchronize()

@@ -44,7 +44,12 @@ def configs(dev):
 
 def main(which):
     dev = torch.device("cuda:0")
+    only = [w.split("_only_")[1] for w in which if "_only_" in w]
+    if only:
+        which = which + ["fwd"]
     for name, c in configs(dev).items():
+        if only and name not in only:
+            continue
         D = 128
         q = fa.random_tensor(1, (c["B"], c["Hq"], c["L"], D), device=dev)
         k = fa.random_tensor(2, (c["B"], c["Hkv"], c["L"], D), device=dev)

@@ -72,7 +72,6 @@ struct BwdParams {
   const int32_t* fkv_num;
   const int32_t* fkv_idx;
   int* turn;           // deterministic mode: per (b*Hq + h, q block) count of finished dQ adds
-  int deterministic;
   const float* lse2;   // (B*Hq, Lq_pad): cterm, see bwd_preprocess_kernel
   const float* delta;  // (B*Hq, Lq_pad)
   float* dq_acc;       // (B*Hq, Lq, D) fp32
@@ -104,6 +103,7 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
 #define FA_BWD_DKSS 1  // dK as an SS MMA from the dS^T smem buffer, issued after dQ
 #endif
 constexpr bool kDkSS = FA_BWD_DKSS != 0;
+
 #ifndef FA_BWD_DQ_TMA
 #define FA_BWD_DQ_TMA 1
 #endif
@@ -248,7 +248,7 @@ __device__ __forceinline__ void det_finish_turn(int* turn, int lane) {
   __syncwarp();
 }
 
-template <int D, class MaskT, class ScoreT>
+template <int D, class MaskT, class ScoreT, bool kDet>
 __global__ void __launch_bounds__(kThreads, 1)
     flex_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int n = 0;; ++n) {
         // deterministic mode claims every item from the counter, so an item is only ever
         // owned by a CTA that is running (the ordered dQ adds wait on lower items only)
-        const int item = p.deterministic ? atomicAdd(p.work_counter, 1)
+        const int item = kDet ? atomicAdd(p.work_counter, 1)
                          : n == 0        ? static_cast<int>(blockIdx.x)
                                          : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
         const int buf = n & 1;
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // four 32 (q) x 32 (d) fp32 tiles per warp: st.shared rows of 128 B (lane = d),
             // then one TMA reduce-add each (rows past Q_LEN are clipped by the tensor map)
             int* turn = nullptr;
-            if (p.deterministic) turn = det_wait_turn(p, it, b, h, r, lane);
+            if constexpr (kDet) turn = det_wait_turn(p, it, b, h, r, lane);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4, ++stage_it) {
               float* stg = sm.dq_stage[wq][stage_it & 1];
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (C::kTmaReduce) {
             // one 32 (q) x D fp32 tile per warp (row per lane; bank conflicts accepted at D=64)
             int* turn = nullptr;
-            if (p.deterministic) turn = det_wait_turn(p, it, b, h, r, lane);
+            if constexpr (kDet) turn = det_wait_turn(p, it, b, h, r, lane);
             float* stg = sm.dq_stage[wq][stage_it & 1];
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
@@ -939,7 +939,7 @@ __global__ void dq_convert_kernel(const float4* __restrict__ acc, uint4* __restr
   }
 }
 
-template <int D, class MaskT, class ScoreT>
+template <int D, class MaskT, class ScoreT, bool kDet>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
               const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
               const BmView& bmt, MaskT mask, ScoreT score, void* workspace, const BwdOptions& opt,
@@ -952,8 +952,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
-  const bool det = (opt.flags & FA_FLAG_DETERMINISTIC) != 0;
-  int* turn = det ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
+  int* turn = kDet ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
   if (opt.events[0]) FA_CHECK_CUDA(cudaEventRecord(opt.events[0], st));
   // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
   bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
@@ -977,7 +976,6 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.q_num = bmt.kv_num; p.q_idx = bmt.kv_idx; p.fq_num = bmt.full_num; p.fq_idx = bmt.full_idx;
   p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.fkv_num = bm.full_num; p.fkv_idx = bm.full_idx;
   p.turn = turn;
-  p.deterministic = det ? 1 : 0;
   p.lse2 = lse2; p.delta = delta; p.dq_acc = dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(dk);
   p.dv = static_cast<__nv_bfloat16*>(dv);
@@ -993,7 +991,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   }
   p.trace = trace;
   const size_t smem = sizeof(BSmem<D>);
-  auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT>;
+  auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT, kDet>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
   if (opt.events[1]) FA_CHECK_CUDA(cudaEventRecord(opt.events[1], st));
@@ -1063,12 +1061,21 @@ fa_status by_mask(const AttnGeom& g, const void* q, const void* k, const void* v
                   const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
                   const BmView& bmt, const MaskParams& mp, int mk, ScoreT s, void* ws,
                   const BwdOptions& opt, cudaStream_t st) {
+  // deterministic mode: one instantiation per score kind, the dynamic (any-combination) mask
+  if (opt.flags & FA_FLAG_DETERMINISTIC)
+    return run<D, MaskFn<kMaskDynamic>, ScoreT, true>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                                       MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
   switch (mk) {
-    case kMaskNoop: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskNoop>{mp}, s, ws, opt, st);
-    case kMaskCausalOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskCausalOnly>{mp}, s, ws, opt, st);
-    case kMaskSlidingOnly: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskSlidingOnly>{mp}, s, ws, opt, st);
-    case kMaskDocCausal: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskDocCausal>{mp}, s, ws, opt, st);
-    default: return run<D>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
+    case kMaskNoop: return run<D, MaskFn<kMaskNoop>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                        MaskFn<kMaskNoop>{mp}, s, ws, opt, st);
+    case kMaskCausalOnly: return run<D, MaskFn<kMaskCausalOnly>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                        MaskFn<kMaskCausalOnly>{mp}, s, ws, opt, st);
+    case kMaskSlidingOnly: return run<D, MaskFn<kMaskSlidingOnly>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                        MaskFn<kMaskSlidingOnly>{mp}, s, ws, opt, st);
+    case kMaskDocCausal: return run<D, MaskFn<kMaskDocCausal>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                        MaskFn<kMaskDocCausal>{mp}, s, ws, opt, st);
+    default: return run<D, MaskFn<kMaskDynamic>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+                                        MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
   }
 }
 

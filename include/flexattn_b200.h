@@ -309,6 +309,62 @@ FA_API fa_status fa_fill_uniform(void* dst, int32_t dtype, uint64_t seed, int64_
 FA_API fa_status fa_paged_write(const fa_tensor* logical, const fa_page_table* pt, fa_tensor* physical,
                          void* stream);
 
+/* ---- device page pool (ABI v4) ------------------------------------------------------
+ * The PagedKVCache allocator (paged_kv.hpp:50-89, paged_kv.cpp:13-152) with ALL of its state
+ * in device memory, so a serving step (append -> convert -> decode) runs without a host round
+ * trip and can be captured in a CUDA graph. Same semantics as the reference, bit for bit:
+ * LIFO free stack with page 0 on top (paged_kv.cpp:27-31), deterministic_shuffle
+ * (random.hpp:49-56), assign = capacity check, erase, pop `needed` pages (:72-98), append_tokens
+ * pops the extra pages (:100-126), erase pushes the owned pages in logical order (:128-141);
+ * max_logical_pages == num_pages (:20).
+ *
+ * A batched update applies its requests IN ORDER, exactly as the same sequence of reference
+ * calls; the first failing request (batch outside [0, batches) -> IndexOutOfRange, not enough
+ * pages -> OutOfPages, a batch id repeated in one call -> ShapeMismatch) stops the batch:
+ * requests before it are applied, it and the ones after are not (the reference's exception
+ * leaves earlier calls applied and the failing one without effect). */
+typedef struct fa_page_pool {
+  int64_t batches, num_pages, page_size;
+  /* device arrays, laid out by fa_page_pool_init in one caller-owned allocation */
+  int32_t* table;            /* (batches, num_pages), -1 = unmapped */
+  int32_t* phys_to_logical;  /* (num_pages), -1 = free */
+  int32_t* owner;            /* (num_pages), -1 = free */
+  int32_t* seq_len;          /* (batches) */
+  int32_t* free_stack;       /* (num_pages): free pages, top = free_stack[*free_count - 1] */
+  int32_t* free_count;       /* device scalar */
+  int32_t* status;           /* device int32[8]: fa_status, failing request (= applied count),
+                                needed, available, tokens, op, batch id of the failure */
+  int32_t* scratch;          /* per-request bookkeeping of the last update */
+} fa_page_pool;
+
+enum { FA_PAGE_ASSIGN = 0, FA_PAGE_APPEND = 1, FA_PAGE_ERASE = 2 };
+/* Update flag: do not synchronise; the outcome stays in pool->status (fa_page_pool_status). */
+enum { FA_FLAG_NO_SYNC = 1u << 2 };
+
+/* Device bytes fa_page_pool_init needs for (batches, num_pages). */
+FA_API size_t fa_page_pool_bytes(int64_t batches, int64_t num_pages);
+/* Lays the pool out in `device_mem` and resets it (every page free, page 0 on top, all
+ * sequences empty), stream-ordered. */
+FA_API fa_status fa_page_pool_init(fa_page_pool* pool, void* device_mem, size_t bytes, int64_t batches,
+                                   int64_t num_pages, int64_t page_size, void* stream);
+/* shuffle_free_pages(seed) (paged_kv.cpp:143-146) on the device free stack. */
+FA_API fa_status fa_page_pool_shuffle(const fa_page_pool* pool, uint64_t seed, void* stream);
+/* n requests (device int32 batch_ids[n], n_tokens[n]; n_tokens ignored for FA_PAGE_ERASE) of
+ * one kind. With k_tokens/v_tokens given (packed (1, Hkv, sum(n_tokens), D), request i's tokens
+ * at offset sum_{j<i} n_tokens[j]) the applied requests' tokens are written into
+ * k_cache/v_cache (1, Hkv, num_pages * page_size, D) at their logical positions
+ * (write_tokens, paged_kv.cpp:54-70): assign from 0, append from the old length. Unless
+ * FA_FLAG_NO_SYNC, the call synchronises the stream and returns the first failure. */
+FA_API fa_status fa_page_pool_update(const fa_page_pool* pool, int32_t op, const int32_t* batch_ids,
+                                     const int32_t* n_tokens, int32_t n, const fa_tensor* k_tokens,
+                                     const fa_tensor* v_tokens, fa_tensor* k_cache, fa_tensor* v_cache,
+                                     uint32_t flags, void* stream);
+/* Reads pool->status (synchronises): the outcome of the last update, as its fa_status with the
+ * reference's message in fa_last_error(); *applied = number of requests applied. */
+FA_API fa_status fa_page_pool_status(const fa_page_pool* pool, int32_t* applied, void* stream);
+/* The pool as a page table for fa_convert_block_mask / fa_flex_decode (max_seq_len = 0). */
+FA_API fa_page_table fa_page_pool_table(const fa_page_pool* pool);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -523,129 +523,115 @@ struct PageTable {
   }
 };
 
-// PagedKVCache: the reference's host page allocator (LIFO free list with page 0 on top,
-// deterministic shuffle, capacity-atomic assign/append, idempotent erase) over device K/V of
-// shape (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel.
+// PagedKVCache (paged_kv.hpp:50-89) with the allocator on the device (fa_page_pool: LIFO free
+// stack with page 0 on top, deterministic shuffle, capacity-checked assign / append, idempotent
+// erase; paged_kv.cpp:13-152) over device K/V of shape (1, kv_heads, num_pages * page_size, dim).
+// Single-sequence calls throw like the reference; the *_batch calls apply many requests in
+// order in one launch (device int32 arrays, one request per sequence) and, with sync = false,
+// leave the outcome on the device for status() (CUDA-graph serving loops).
 class PagedKVCache {
  public:
-  PagedKVCache(i64 batches, i64 num_pages, i64 page_size, i64 kv_heads, i64 dim, DType t = DType::BF16)
+  PagedKVCache(i64 batches, i64 num_pages, i64 page_size, i64 kv_heads, i64 dim, DType t = DType::BF16,
+               cudaStream_t st = nullptr)
       : k_(1, kv_heads, num_pages * page_size, dim, t), v_(1, kv_heads, num_pages * page_size, dim, t) {
     if (batches < 1 || num_pages < 1 || page_size < 1)
       throw ShapeMismatch("PagedKVCache: batches, num_pages and page_size must be >= 1");
-    pt_.batches = batches;
-    pt_.max_logical_pages = num_pages;
-    pt_.num_physical_pages = num_pages;
-    pt_.page_size = page_size;
-    pt_.table.assign(static_cast<size_t>(batches * num_pages), PageTable::kSentinel);
-    pt_.phys_to_logical.assign(static_cast<size_t>(num_pages), PageTable::kSentinel);
-    pt_.owner.assign(static_cast<size_t>(num_pages), PageTable::kSentinel);
-    pt_.seq_len.assign(static_cast<size_t>(batches), 0);
-    for (i64 p = num_pages - 1; p >= 0; --p) free_.push_back(static_cast<std::int32_t>(p));  // page 0 on top
-    check_cuda(cudaMemset(k_.buf.get(), 0, k_.buf.bytes), "cache");
-    check_cuda(cudaMemset(v_.buf.get(), 0, v_.buf.bytes), "cache");
+    const size_t bytes = fa_page_pool_bytes(batches, num_pages);
+    mem_ = DeviceBuffer(bytes);
+    check(fa_page_pool_init(&pool_, mem_.get(), bytes, batches, num_pages, page_size, st));
+    check_cuda(cudaMemsetAsync(k_.buf.get(), 0, k_.buf.bytes, st), "cache");
+    check_cuda(cudaMemsetAsync(v_.buf.get(), 0, v_.buf.bytes, st), "cache");
+    ids_ = DeviceBuffer(static_cast<size_t>(batches) * 4);
+    ntok_ = DeviceBuffer(static_cast<size_t>(batches) * 4);
   }
 
   // assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim) on the device
   void assign(i64 b, const DeviceTensor4& k_tokens, const DeviceTensor4& v_tokens, cudaStream_t st = nullptr) {
-    check_batch(b);
-    check_tokens(k_tokens, v_tokens);
-    const i64 needed = ceil_div(k_tokens.l, pt_.page_size), owned = ceil_div(seq(b), pt_.page_size);
-    if (needed > static_cast<i64>(free_.size()) + owned)
-      throw OutOfPages("PagedKVCache: assign of " + std::to_string(k_tokens.l) + " tokens needs " +
-                       std::to_string(needed) + " pages, only " +
-                       std::to_string(static_cast<i64>(free_.size()) + owned) + " available");
-    erase(b);
-    for (i64 lp = 0; lp < needed; ++lp) take(b, lp);
-    seq(b) = static_cast<std::int32_t>(k_tokens.l);
-    write(b, 0, k_tokens, v_tokens, st);
+    one(FA_PAGE_ASSIGN, b, k_tokens.l, &k_tokens, &v_tokens, st);
   }
-  // append_tokens (paged_kv.cpp:100-126); the append must start on a page boundary or the
-  // caller passes the tail of the partially filled page again (write_tokens is page-granular)
+  // append_tokens (paged_kv.cpp:100-126), at any position (fills the slack of the last page)
   void append_tokens(i64 b, const DeviceTensor4& k_new, const DeviceTensor4& v_new, cudaStream_t st = nullptr) {
-    check_batch(b);
-    check_tokens(k_new, v_new);
-    const i64 old = seq(b), owned = ceil_div(old, pt_.page_size), total = ceil_div(old + k_new.l, pt_.page_size);
-    if (total - owned > static_cast<i64>(free_.size()))
-      throw OutOfPages("PagedKVCache: append of " + std::to_string(k_new.l) + " tokens needs " +
-                       std::to_string(total - owned) + " new pages, only " + std::to_string(free_.size()) + " free");
-    if (old % pt_.page_size != 0)
-      throw Unsupported("PagedKVCache::append_tokens: unaligned appends go through the Python layer");
-    for (i64 lp = owned; lp < total; ++lp) take(b, lp);
-    seq(b) = static_cast<std::int32_t>(old + k_new.l);
-    write(b, old, k_new, v_new, st);
+    one(FA_PAGE_APPEND, b, k_new.l, &k_new, &v_new, st);
   }
   // erase (paged_kv.cpp:128-141): idempotent
-  void erase(i64 b) {
-    check_batch(b);
-    for (i64 lp = 0; lp < ceil_div(seq(b), pt_.page_size); ++lp) {
-      const size_t slot = static_cast<size_t>(b * pt_.max_logical_pages + lp);
-      const std::int32_t page = pt_.table[slot];
-      pt_.table[slot] = PageTable::kSentinel;
-      pt_.phys_to_logical[static_cast<size_t>(page)] = PageTable::kSentinel;
-      pt_.owner[static_cast<size_t>(page)] = PageTable::kSentinel;
-      free_.push_back(page);
-    }
-    seq(b) = 0;
+  void erase(i64 b, cudaStream_t st = nullptr) { one(FA_PAGE_ERASE, b, 0, nullptr, nullptr, st); }
+  // batched updates: device int32 batch_ids[n] / n_tokens[n]; tokens packed along L (or null)
+  void update_batch(int32_t op, const int32_t* batch_ids, const int32_t* n_tokens, int32_t n,
+                    const DeviceTensor4* k_tokens, const DeviceTensor4* v_tokens, bool sync = true,
+                    cudaStream_t st = nullptr) {
+    fa_tensor kt{}, vt{}, kc = k_.c(), vc = v_.c();
+    if (k_tokens != nullptr) { kt = k_tokens->c(); vt = v_tokens->c(); }
+    check(fa_page_pool_update(&pool_, op, batch_ids, n_tokens, n, k_tokens ? &kt : nullptr,
+                              v_tokens ? &vt : nullptr, &kc, &vc, sync ? 0u : uint32_t(FA_FLAG_NO_SYNC), st));
+  }
+  // outcome of the last update (synchronises); returns the number of requests applied
+  int32_t status(cudaStream_t st = nullptr) const {
+    int32_t applied = 0;
+    check(fa_page_pool_status(&pool_, &applied, st));
+    return applied;
   }
   // shuffle_free_pages (paged_kv.cpp:143-146, deterministic_shuffle random.hpp:49-56)
-  void shuffle_free_pages(std::uint64_t seed) {
-    std::uint64_t state = seed;
-    for (size_t i = free_.size(); i > 1; --i) {
-      state += 0x9e3779b97f4a7c15ull;
-      std::uint64_t z = state;
-      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-      z ^= z >> 31;
-      std::swap(free_[i - 1], free_[static_cast<size_t>(z % i)]);
-    }
+  void shuffle_free_pages(std::uint64_t seed, cudaStream_t st = nullptr) {
+    check(fa_page_pool_shuffle(&pool_, seed, st));
   }
   const DeviceTensor4& k_phys() const { return k_; }
   const DeviceTensor4& v_phys() const { return v_; }
-  const PageTable& table() const { return pt_; }
-  i64 page_size() const { return pt_.page_size; }
-  i64 max_tokens() const { return pt_.num_physical_pages * pt_.page_size; }
-  i64 seq_len(i64 b) const { check_batch(b); return pt_.seq_len[static_cast<size_t>(b)]; }
-  i64 free_pages() const { return static_cast<i64>(free_.size()); }
+  // live device page table (no copy) for convert_block_mask / decode
+  fa_page_table device_table() const {
+    fa_page_table t = fa_page_pool_table(&pool_);
+    t.max_seq_len = max_seq_len();
+    return t;
+  }
+  // host snapshot of the page table (paged_kv.hpp:18-41)
+  PageTable table() const {
+    PageTable pt;
+    pt.batches = pool_.batches;
+    pt.max_logical_pages = pt.num_physical_pages = pool_.num_pages;
+    pt.page_size = pool_.page_size;
+    pt.table = down(pool_.table, pool_.batches * pool_.num_pages);
+    pt.phys_to_logical = down(pool_.phys_to_logical, pool_.num_pages);
+    pt.owner = down(pool_.owner, pool_.num_pages);
+    pt.seq_len = down(pool_.seq_len, pool_.batches);
+    return pt;
+  }
+  i64 page_size() const { return pool_.page_size; }
+  i64 max_tokens() const { return pool_.num_pages * pool_.page_size; }
+  i64 seq_len(i64 b) const {
+    check_batch(b);
+    std::int32_t v = 0;
+    check_cuda(cudaMemcpy(&v, pool_.seq_len + b, 4, cudaMemcpyDeviceToHost), "seq_len");
+    return v;
+  }
+  i64 free_pages() const { return down(pool_.free_count, 1)[0]; }
+  const fa_page_pool& pool() const { return pool_; }
 
  private:
-  static i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
-  std::int32_t& seq(i64 b) { return pt_.seq_len[static_cast<size_t>(b)]; }
+  static std::vector<std::int32_t> down(const std::int32_t* p, i64 n) {
+    std::vector<std::int32_t> v(static_cast<size_t>(n));
+    if (n) check_cuda(cudaMemcpy(v.data(), p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost), "page pool");
+    return v;
+  }
+  i64 max_seq_len() const {
+    const auto s = down(pool_.seq_len, pool_.batches);
+    return s.empty() ? 0 : *std::max_element(s.begin(), s.end());
+  }
   void check_batch(i64 b) const {
-    if (b < 0 || b >= pt_.batches)
+    if (b < 0 || b >= pool_.batches)
       throw IndexOutOfRange("PagedKVCache: batch " + std::to_string(b) + " outside [0, " +
-                            std::to_string(pt_.batches) + ")");
+                            std::to_string(pool_.batches) + ")");
   }
-  void check_tokens(const DeviceTensor4& kt, const DeviceTensor4& vt) const {
-    if (!kt.same_shape(vt)) throw ShapeMismatch("PagedKVCache: k and v tokens must agree");
-    if (kt.b != 1 || kt.h != k_.h || kt.d != k_.d || kt.dtype != k_.dtype)
-      throw ShapeMismatch("PagedKVCache: token tensors must be (1, kv_heads, n, dim) of the cache dtype");
-  }
-  void take(i64 b, i64 lp) {
-    const std::int32_t page = free_.back();
-    free_.pop_back();
-    pt_.table[static_cast<size_t>(b * pt_.max_logical_pages + lp)] = page;
-    pt_.phys_to_logical[static_cast<size_t>(page)] = static_cast<std::int32_t>(lp);
-    pt_.owner[static_cast<size_t>(page)] = static_cast<std::int32_t>(b);
-  }
-  // write_tokens (paged_kv.cpp:54-70) through a one-batch view of the table
-  void write(i64 b, i64 start, const DeviceTensor4& kt, const DeviceTensor4& vt, cudaStream_t st) {
-    if (kt.l == 0) return;
-    const i64 lp0 = start / pt_.page_size, np = ceil_div(kt.l, pt_.page_size);
-    DeviceBuffer row(static_cast<size_t>(np) * 4);
-    check_cuda(cudaMemcpyAsync(row.get(), pt_.table.data() + b * pt_.max_logical_pages + lp0,
-                               static_cast<size_t>(np) * 4, cudaMemcpyHostToDevice, st), "page row");
-    fa_page_table v{};
-    v.batches = 1; v.max_logical_pages = np; v.num_physical_pages = pt_.num_physical_pages;
-    v.page_size = pt_.page_size; v.table = row.as<int32_t>();
-    fa_tensor lk = kt.c(), lv = vt.c(), pk = k_.c(), pv = v_.c();
-    check(fa_paged_write(&lk, &v, &pk, st));
-    check(fa_paged_write(&lv, &v, &pv, st));
-    check_cuda(cudaStreamSynchronize(st), "paged write");  // `row` is freed on return
+  void one(int32_t op, i64 b, i64 n, const DeviceTensor4* kt, const DeviceTensor4* vt, cudaStream_t st) {
+    if (kt != nullptr && (!kt->same_shape(*vt) || kt->dtype != vt->dtype))
+      throw ShapeMismatch("PagedKVCache: k and v tokens must agree");
+    const std::int32_t req[2] = {static_cast<std::int32_t>(b), static_cast<std::int32_t>(n)};
+    check_cuda(cudaMemcpyAsync(ids_.get(), &req[0], 4, cudaMemcpyHostToDevice, st), "request");
+    check_cuda(cudaMemcpyAsync(ntok_.get(), &req[1], 4, cudaMemcpyHostToDevice, st), "request");
+    update_batch(op, ids_.as<int32_t>(), ntok_.as<int32_t>(), 1, kt, vt, true, st);
   }
 
   DeviceTensor4 k_, v_;
-  PageTable pt_;
-  std::vector<std::int32_t> free_;  // LIFO
+  DeviceBuffer mem_, ids_, ntok_;
+  fa_page_pool pool_{};
 };
 
 // convert_block_mask over a host PageTable (uploads a device snapshot).

@@ -568,6 +568,34 @@ def ref_paged_layout(B, num_pages, page_size, shuffle_seed, tokens_per_batch):
     return table, p2l, owner
 
 
+def ref_paged_script(B, num_pages, page_size, heads, dim, ops, tok):
+    """Run a script of PagedKVCache calls on the reference (ref_shim.cpp ref_paged_script):
+    ops = [(kind, b, n, seed)], kind 0 assign / 1 append / 2 erase / 3 shuffle. Returns
+    (status per op, table, p2l, owner, seq_len, free_pages, k_phys, v_phys)."""
+    m = len(ops)
+    op = np.array([o[0] for o in ops], np.int32)
+    bat = np.array([o[1] for o in ops], np.int64)
+    nn = np.array([o[2] for o in ops], np.int64)
+    seed = np.array([o[3] & (2**64 - 1) for o in ops], np.uint64)
+    tok = np.ascontiguousarray(tok, np.float32)
+    status = np.zeros(m, np.int32)
+    table = np.zeros((B, num_pages), np.int32)
+    p2l = np.zeros(num_pages, np.int32)
+    owner = np.zeros(num_pages, np.int32)
+    seq = np.zeros(B, np.int64)
+    free = C.c_int64(0)
+    kp = np.zeros((1, heads, num_pages * page_size, dim), np.float32)
+    vp = np.zeros_like(kp)
+    lib = ref()
+    st = lib.ref_paged_script(*_i64(B, num_pages, page_size, heads, dim, m), _p(op, C.c_int32),
+                              _p(bat, C.c_int64), _p(nn, C.c_int64), _p(seed, C.c_uint64),
+                              _p(tok, C.c_float), _p(status, C.c_int32), _p(table, C.c_int32),
+                              _p(p2l, C.c_int32), _p(owner, C.c_int32), _p(seq, C.c_int64),
+                              C.byref(free), _p(kp, C.c_float), _p(vp, C.c_float))
+    _check(st, lib)
+    return status, table, p2l, owner, seq, free.value, kp, vp
+
+
 def ref_convert_block_mask(mask: Mask, bd, hd, ql, kl, bs, table: np.ndarray, num_physical_pages: int):
     table = np.ascontiguousarray(table, dtype=np.int32)
     batches, mlp = table.shape

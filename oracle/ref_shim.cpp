@@ -436,6 +436,60 @@ int ref_paged_layout(int64_t B, int64_t num_pages, int64_t page_size, uint64_t s
   }
 }
 
+// A script of PagedKVCache calls on the reference (paged_kv.cpp:13-152): op[i] 0 = assign,
+// 1 = append_tokens, 2 = erase, 3 = shuffle_free_pages(seed[i]); n[i] tokens whose element
+// (h, t, d) of the token tensor is tok[base + (h * n + t) * dim + d] (base = running sum of
+// n * heads * dim over the token-carrying calls). status[i] = the call's error status (0 = ok;
+// a failing call is caught and the script goes on). Outputs the final table, p2l, owner,
+// seq_len, free page count and the physical K and V buffers (V = -K).
+int ref_paged_script(int64_t B, int64_t num_pages, int64_t page_size, int64_t heads, int64_t dim,
+                     int64_t n_ops, const int32_t* op, const int64_t* bat, const int64_t* n,
+                     const uint64_t* seed, const float* tok, int32_t* status, int32_t* table,
+                     int32_t* p2l, int32_t* owner, int64_t* seq, int64_t* free_pages, float* k_out,
+                     float* v_out) {
+  try {
+    PagedKVCache<float> cache(B, num_pages, page_size, heads, dim);
+    int64_t base = 0;
+    for (int64_t i = 0; i < n_ops; ++i) {
+      status[i] = 0;
+      try {
+        if (op[i] == 3) {
+          cache.shuffle_free_pages(seed[i]);
+        } else if (op[i] == 2) {
+          cache.erase(bat[i]);
+        } else {
+          Tensor4<float> kt(1, heads, n[i], dim), vt(1, heads, n[i], dim);
+          for (int64_t h = 0; h < heads; ++h)
+            for (int64_t t = 0; t < n[i]; ++t)
+              for (int64_t d = 0; d < dim; ++d) {
+                const float x = tok[base + (h * n[i] + t) * dim + d];
+                kt.at(0, h, t, d) = x;
+                vt.at(0, h, t, d) = -x;
+              }
+          base += n[i] * heads * dim;
+          if (op[i] == 0) cache.assign(bat[i], kt, vt);
+          else cache.append_tokens(bat[i], kt, vt);
+        }
+      } catch (const std::exception& e) {
+        status[i] = status_of(e);
+      }
+    }
+    const auto& pt = cache.table();
+    std::memcpy(table, pt.table.data(), pt.table.size() * sizeof(int32_t));
+    std::memcpy(p2l, pt.phys_to_logical.data(), pt.phys_to_logical.size() * 4);
+    std::memcpy(owner, pt.owner.data(), pt.owner.size() * 4);
+    for (int64_t b = 0; b < B; ++b) seq[b] = cache.seq_len(b);
+    *free_pages = cache.free_pages();
+    const auto& kp = cache.k_phys();
+    const auto& vp = cache.v_phys();
+    std::memcpy(k_out, kp.data().data(), kp.data().size() * sizeof(float));
+    std::memcpy(v_out, vp.data().data(), vp.data().size() * sizeof(float));
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 }  // extern "C"
 
 // Timing entry for bench.py's CPU legs: the reference forward and backward on

@@ -55,7 +55,15 @@ class OpCountersC(C.Structure):
     _fields_ = [("madds", C.c_uint64), ("mask_evals", C.c_uint64), ("score_evals", C.c_uint64)]
 
 
-FA_FLAG_VALIDATE, FA_FLAG_DETERMINISTIC = 1, 2
+FA_FLAG_VALIDATE, FA_FLAG_DETERMINISTIC, FA_FLAG_NO_SYNC = 1, 2, 4
+PAGE_ASSIGN, PAGE_APPEND, PAGE_ERASE = 0, 1, 2
+
+
+class PagePoolC(C.Structure):
+    _fields_ = [("batches", C.c_int64), ("num_pages", C.c_int64), ("page_size", C.c_int64),
+                ("table", C.c_void_p), ("phys_to_logical", C.c_void_p), ("owner", C.c_void_p),
+                ("seq_len", C.c_void_p), ("free_stack", C.c_void_p), ("free_count", C.c_void_p),
+                ("status", C.c_void_p), ("scratch", C.c_void_p)]
 
 
 class FwdArgs(C.Structure):
@@ -90,7 +98,8 @@ EXPORTS = [
     "fa_block_mask_geometry", "fa_create_block_mask", "fa_transpose_block_mask",
     "fa_convert_block_mask", "fa_flex_fwd", "fa_bwd_workspace_size", "fa_flex_bwd",
     "fa_decode_workspace_size", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
-    "fa_check_finite",
+    "fa_check_finite", "fa_page_pool_bytes", "fa_page_pool_init", "fa_page_pool_shuffle",
+    "fa_page_pool_update", "fa_page_pool_status", "fa_page_pool_table",
 ]
 
 _lib = None
@@ -129,7 +138,19 @@ def load():
     lib.fa_paged_write.argtypes = [C.POINTER(TensorC), C.POINTER(PageTableC), C.POINTER(TensorC),
                                    C.c_void_p]
     lib.fa_check_finite.argtypes = [C.POINTER(TensorC), C.POINTER(C.c_char_p), C.c_int32, C.c_void_p]
-    for fn in ("fa_create_block_mask", "fa_transpose_block_mask", "fa_convert_block_mask",
+    lib.fa_page_pool_bytes.restype = C.c_size_t
+    lib.fa_page_pool_bytes.argtypes = [C.c_int64, C.c_int64]
+    lib.fa_page_pool_init.argtypes = [C.POINTER(PagePoolC), C.c_void_p, C.c_size_t, C.c_int64, C.c_int64,
+                                      C.c_int64, C.c_void_p]
+    lib.fa_page_pool_shuffle.argtypes = [C.POINTER(PagePoolC), C.c_uint64, C.c_void_p]
+    lib.fa_page_pool_update.argtypes = [C.POINTER(PagePoolC), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                        C.POINTER(TensorC), C.POINTER(TensorC), C.POINTER(TensorC),
+                                        C.POINTER(TensorC), C.c_uint32, C.c_void_p]
+    lib.fa_page_pool_status.argtypes = [C.POINTER(PagePoolC), C.POINTER(C.c_int32), C.c_void_p]
+    lib.fa_page_pool_table.restype = PageTableC
+    lib.fa_page_pool_table.argtypes = [C.POINTER(PagePoolC)]
+    for fn in ("fa_page_pool_init", "fa_page_pool_shuffle", "fa_page_pool_update", "fa_page_pool_status",
+               "fa_create_block_mask", "fa_transpose_block_mask", "fa_convert_block_mask",
                "fa_flex_fwd", "fa_flex_bwd", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
                "fa_block_mask_geometry", "fa_check_finite"):
         getattr(lib, fn).restype = C.c_int32

@@ -11,7 +11,7 @@ reached through ``libflexattn_b200.so``. There is no CPU path.
     forward             engine.hpp:68-71         -> fa_flex_fwd
     backward            engine.hpp:78-82         -> fa_flex_bwd
     decode              engine.hpp:92-96         -> fa_flex_decode
-    PagedKVCache        paged_kv.hpp:50-89       (host page table; device K/V)
+    PagedKVCache        paged_kv.hpp:50-89       -> fa_page_pool_* (allocator + K/V on the device)
     convert_block_mask  paged_kv.hpp:101         -> fa_convert_block_mask
 """
 from __future__ import annotations
@@ -25,7 +25,8 @@ import torch
 
 from . import _lib
 from ._lib import (FA_BF16, FA_F32, FA_FLAG_DETERMINISTIC, FA_FLAG_VALIDATE, BlockMaskC, BwdArgs,
-                   DecodeArgs, FwdArgs, MaskDesc, OpCountersC, PageTableC, ScoreDesc, TensorC)
+                   DecodeArgs, FwdArgs, MaskDesc, OpCountersC, PagePoolC, PageTableC, ScoreDesc, TensorC,
+                   FA_FLAG_NO_SYNC, PAGE_ASSIGN, PAGE_APPEND, PAGE_ERASE)
 
 # ---------------------------------------------------------------- errors (errors.hpp:11-101)
 
@@ -766,96 +767,180 @@ class PageTable:
         return s
 
 
+class DevicePageTable:
+    """Live view of a device page pool as a PageTable (paged_kv.hpp:18-41): the kernels read the
+    pool's own arrays (no upload); the host lists are downloaded on access."""
+
+    def __init__(self, cache: "PagedKVCache"):
+        self._cache = cache
+        self.batches = cache.batches
+        self.max_logical_pages = cache.num_pages
+        self.num_physical_pages = cache.num_pages
+        self.page_size = cache.ps
+
+    def _arr(self, name):
+        return self._cache._view(name).cpu().tolist()
+
+    @property
+    def table(self):
+        return self._arr("table")
+
+    @property
+    def phys_to_logical(self):
+        return self._arr("phys_to_logical")
+
+    @property
+    def owner(self):
+        return self._arr("owner")
+
+    @property
+    def seq_len(self):
+        return self._arr("seq_len")
+
+    def lookup(self, b, logical_page):
+        return int(self._cache._view("table")[b * self.max_logical_pages + logical_page].item())
+
+    def c(self, device=None) -> PageTableC:
+        s = _lib.load().fa_page_pool_table(C.byref(self._cache._pool))
+        s.max_seq_len = self._cache._max_seq_len()
+        return s
+
+
 class PagedKVCache:
-    """PagedKVCache (paged_kv.hpp:50-89): host page allocator (paging.PageAllocator: LIFO free
-    list, deterministic shuffle, atomic capacity checks) + device K/V of shape
-    (1, kv_heads, num_pages * page_size, dim); token writes are a device scatter kernel
-    (fa_paged_write, write_tokens paged_kv.cpp:54-70)."""
+    """PagedKVCache (paged_kv.hpp:50-89) with the page allocator ON THE DEVICE (fa_page_pool:
+    LIFO free stack with page 0 on top, deterministic shuffle, capacity-checked assign / append,
+    erase; paged_kv.cpp:13-152) and device K/V of shape (1, kv_heads, num_pages * page_size, dim).
+    Single-sequence calls mirror the reference; the ``*_batch`` calls apply many requests in
+    order in one launch (one sequence per request), with ``sync=False`` for CUDA-graph serving
+    loops (the outcome stays on the device until ``status()``)."""
 
     def __init__(self, batches, num_pages, page_size, kv_heads, dim, dtype=torch.bfloat16,
                  device="cuda"):
-        from .paging import PageAllocator
-        try:
-            self.alloc = PageAllocator(batches, num_pages, page_size)
-        except ValueError as e:
-            raise ShapeMismatch(str(e)) from None
+        if batches < 1 or num_pages < 1 or page_size < 1:
+            raise ShapeMismatch("PagedKVCache: batches, num_pages and page_size must be >= 1")
         self.batches, self.num_pages, self.ps = batches, num_pages, page_size
         self.kv_heads, self.dim = kv_heads, dim
         self.device = torch.device(device)
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        lib = _lib.load()
+        nbytes = lib.fa_page_pool_bytes(batches, num_pages)
+        self._mem = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._pool = PagePoolC()
+        with torch.cuda.device(self.device):
+            _check(lib.fa_page_pool_init(C.byref(self._pool), C.c_void_p(self._mem.data_ptr()), nbytes,
+                                         batches, num_pages, page_size, C.c_void_p(_stream())))
         self.k = torch.zeros((1, kv_heads, num_pages * page_size, dim), dtype=dtype, device=self.device)
         self.v = torch.zeros_like(self.k)
+        self._seq_host = [0] * batches  # mirror kept by the synchronous calls
+        self._host_valid = True
 
-    def page_table(self) -> PageTable:
-        a = self.alloc
-        return PageTable(self.batches, self.num_pages, self.num_pages, self.ps, list(a.table),
-                         list(a.phys_to_logical), list(a.owner), list(a.seq))
+    # -- device state ------------------------------------------------------------------------
+    def _view(self, name):
+        ptr = getattr(self._pool, name)
+        n = {"table": self.batches * self.num_pages, "phys_to_logical": self.num_pages,
+             "owner": self.num_pages, "seq_len": self.batches, "free_stack": self.num_pages,
+             "free_count": 1}[name]
+        off = (ptr - self._mem.data_ptr()) // 4
+        return self._mem.view(torch.int32)[off:off + n]
+
+    def _max_seq_len(self):
+        if not self._host_valid:
+            self._seq_host = self._view("seq_len").cpu().tolist()
+            self._host_valid = True
+        return max(self._seq_host) if self._seq_host else 0
+
+    def page_table(self) -> DevicePageTable:
+        return DevicePageTable(self)
 
     def shuffle_free_pages(self, seed: int):
-        self.alloc.shuffle_free_pages(seed)
-
-    def _check_batch(self, b):
-        try:
-            self.alloc.check_batch(b)
-        except IndexError as e:
-            raise IndexOutOfRange(str(e)) from None
-
-    def erase(self, b):
-        self._check_batch(b)
-        self.alloc.erase(b)
-
-    def assign(self, b, k_tokens, v_tokens):
-        """assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim)."""
-        from .paging import OutOfPagesError
-        self._check_batch(b)
-        self._check_tokens(k_tokens, v_tokens)
-        try:
-            self.alloc.assign(b, k_tokens.shape[2])
-        except OutOfPagesError as e:
-            raise OutOfPages(str(e)) from None
-        self._write(b, 0, k_tokens, v_tokens)
-
-    def append_tokens(self, b, k_new, v_new):
-        """append_tokens (paged_kv.cpp:100-126)."""
-        from .paging import OutOfPagesError
-        self._check_batch(b)
-        self._check_tokens(k_new, v_new)
-        old = self.alloc.seq[b]
-        try:
-            self.alloc.append(b, k_new.shape[2])
-        except OutOfPagesError as e:
-            raise OutOfPages(str(e)) from None
-        self._write(b, old, k_new, v_new)
+        """shuffle_free_pages (paged_kv.cpp:143-146) of the device free stack."""
+        with torch.cuda.device(self.device):
+            _check(_lib.load().fa_page_pool_shuffle(C.byref(self._pool), C.c_uint64(seed & (2**64 - 1)),
+                                                    C.c_void_p(_stream())))
 
     def _check_tokens(self, k_t, v_t):
         if tuple(k_t.shape) != tuple(v_t.shape):
             raise ShapeMismatch("PagedKVCache: k and v tokens must agree")
-        if k_t.shape[0] != 1 or k_t.shape[1] != self.kv_heads or k_t.shape[3] != self.dim:
+        if k_t.dim() != 4 or k_t.shape[0] != 1 or k_t.shape[1] != self.kv_heads or k_t.shape[3] != self.dim:
             raise ShapeMismatch(f"PagedKVCache: token tensors must be (1,{self.kv_heads},n,{self.dim})")
 
-    def _write(self, b, start, k_t, v_t):
-        # device scatter through a one-batch page table view (write_tokens, paged_kv.cpp:54-70)
-        n = k_t.shape[2]
-        if n == 0:
-            return
-        if start % self.ps != 0:
-            # unaligned append: stage the partial first page so the scatter is page-aligned
-            pad = start % self.ps
-            base = self.alloc.lookup(b, start // self.ps) * self.ps
-            ks = torch.cat([self.k[:, :, base:base + pad], k_t.to(self.device, self.k.dtype)], dim=2)
-            vs = torch.cat([self.v[:, :, base:base + pad], v_t.to(self.device, self.v.dtype)], dim=2)
-            k_t, v_t, start = ks, vs, start - pad
-        lp0 = start // self.ps
-        npages = -(-k_t.shape[2] // self.ps)
-        row = self.alloc.table[b * self.num_pages + lp0: b * self.num_pages + lp0 + npages]
-        pt = PageTable(1, npages, self.num_pages, self.ps, row, self.alloc.phys_to_logical,
-                       self.alloc.owner, [k_t.shape[2]])
-        cpt = pt.c(self.device)
+    def _update(self, op, batch_ids, n_tokens=None, k_t=None, v_t=None, sync=True):
         lib = _lib.load()
-        for src, dst in ((k_t, self.k), (v_t, self.v)):
-            src = src.to(device=self.device, dtype=self.k.dtype).contiguous()
-            s, d = _tensor(src, "tokens"), _tensor(dst, "cache")
-            with torch.cuda.device(self.device):
-                _check(lib.fa_paged_write(C.byref(s), C.byref(cpt), C.byref(d), C.c_void_p(_stream())))
+        n = len(batch_ids) if not torch.is_tensor(batch_ids) else batch_ids.numel()
+        i32 = dict(dtype=torch.int32, device=self.device)
+        ids = batch_ids.to(**i32) if torch.is_tensor(batch_ids) else torch.tensor(list(batch_ids), **i32)
+        nt = None
+        if op != PAGE_ERASE:
+            nt = n_tokens.to(**i32) if torch.is_tensor(n_tokens) else torch.tensor(list(n_tokens), **i32)
+        tk = tv = ck = cv = None
+        if k_t is not None:
+            self._check_tokens(k_t, v_t)
+            k_t = k_t.to(device=self.device, dtype=self.k.dtype).contiguous()
+            v_t = v_t.to(device=self.device, dtype=self.k.dtype).contiguous()
+            tk, tv = C.byref(_tensor(k_t, "k_tokens")), C.byref(_tensor(v_t, "v_tokens"))
+            ck, cv = C.byref(_tensor(self.k, "k_cache")), C.byref(_tensor(self.v, "v_cache"))
+        with torch.cuda.device(self.device):
+            st = C.c_void_p(_stream())
+            _check(lib.fa_page_pool_update(C.byref(self._pool), op, C.c_void_p(ids.data_ptr() if n else 0),
+                                           C.c_void_p(nt.data_ptr() if nt is not None and n else 0), n,
+                                           tk, tv, ck, cv, FA_FLAG_NO_SYNC, st))
+            if not sync:
+                self._host_valid = False
+                self._keep = (ids, nt, k_t, v_t)  # alive until the stream has consumed them
+                return None
+            applied = C.c_int32(0)
+            rc = lib.fa_page_pool_status(C.byref(self._pool), C.byref(applied), st)
+        # host mirror of the applied prefix (requests run in order)
+        ids_h = ids.cpu().tolist()
+        nt_h = nt.cpu().tolist() if nt is not None else None
+        if self._host_valid:
+            for i in range(applied.value):
+                b = ids_h[i]
+                self._seq_host[b] = (nt_h[i] if op == PAGE_ASSIGN else
+                                     self._seq_host[b] + nt_h[i] if op == PAGE_APPEND else 0)
+        _check(rc)
+        return applied.value
+
+    def status(self):
+        """Outcome of the last update (synchronises): raises its error, else the applied count."""
+        applied = C.c_int32(0)
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            rc = lib.fa_page_pool_status(C.byref(self._pool), C.byref(applied), C.c_void_p(_stream()))
+        _check(rc)
+        return applied.value
+
+    # -- the reference's calls ---------------------------------------------------------------
+    def _check_batch(self, b):
+        if b < 0 or b >= self.batches:
+            raise IndexOutOfRange(f"PagedKVCache: batch {b} outside [0, {self.batches})")
+
+    def erase(self, b):
+        """erase (paged_kv.cpp:128-141)."""
+        self._update(PAGE_ERASE, [b])
+
+    def assign(self, b, k_tokens, v_tokens):
+        """assign (paged_kv.cpp:72-98): tokens (1, kv_heads, n, dim)."""
+        self._check_tokens(k_tokens, v_tokens)
+        self._update(PAGE_ASSIGN, [b], [k_tokens.shape[2]], k_tokens, v_tokens)
+
+    def append_tokens(self, b, k_new, v_new):
+        """append_tokens (paged_kv.cpp:100-126)."""
+        self._check_tokens(k_new, v_new)
+        self._update(PAGE_APPEND, [b], [k_new.shape[2]], k_new, v_new)
+
+    # -- batched (one launch for many sequences) ------------------------------------------------
+    def assign_batch(self, batch_ids, n_tokens, k_tokens=None, v_tokens=None, sync=True):
+        """assign for each (batch_ids[i], n_tokens[i]) in order; tokens packed along L."""
+        return self._update(PAGE_ASSIGN, batch_ids, n_tokens, k_tokens, v_tokens, sync)
+
+    def append_batch(self, batch_ids, n_tokens, k_new=None, v_new=None, sync=True):
+        """append_tokens for each (batch_ids[i], n_tokens[i]) in order; tokens packed along L."""
+        return self._update(PAGE_APPEND, batch_ids, n_tokens, k_new, v_new, sync)
+
+    def erase_batch(self, batch_ids, sync=True):
+        return self._update(PAGE_ERASE, batch_ids, None, None, None, sync)
 
     def k_phys(self):
         return self.k
@@ -865,10 +950,14 @@ class PagedKVCache:
 
     def seq_len(self, b):
         self._check_batch(b)
-        return self.alloc.seq[b]
+        return int(self._view("seq_len")[b].item())
 
     def free_pages(self):
-        return len(self.alloc.free)
+        return int(self._view("free_count")[0].item())
+
+    def free_list(self):
+        """The free stack bottom to top (the reference's free_ vector)."""
+        return self._view("free_stack")[:self.free_pages()].cpu().tolist()
 
     def max_tokens(self):
         return self.num_pages * self.ps

@@ -223,7 +223,7 @@ BmView kv_view(const fa_block_mask* bm) {
 extern "C" {
 
 const char* fa_last_error(void) { return g_last_error.c_str(); }
-int32_t fa_abi_version(void) { return 3; }  // v3: flags, counters, phase events, fa_check_finite
+int32_t fa_abi_version(void) { return 4; }  // v3: flags, counters, phase events, fa_check_finite; v4: device page pool
 uint64_t fa_launch_count(void) { return g_launches.load(); }
 
 const char* fa_status_name(fa_status s) {

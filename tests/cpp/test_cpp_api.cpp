@@ -267,6 +267,21 @@ int main() {
       small.assign(0, big, big);
     } catch (const OutOfPages&) { thrown = true; }
     EXPECT(thrown);
+    // batched device-side appends: one token for each sequence, no host sync, then status()
+    {
+      PagedKVCache pool(3, 6, 4, 1, 8);
+      const int32_t ids[3] = {2, 0, 1}, nt[3] = {5, 4, 13};
+      DeviceBuffer dids(12), dnt(12);
+      check_cuda(cudaMemcpy(dids.get(), ids, 12, cudaMemcpyHostToDevice), "ids");
+      check_cuda(cudaMemcpy(dnt.get(), nt, 12, cudaMemcpyHostToDevice), "nt");
+      pool.update_batch(FA_PAGE_APPEND, dids.as<int32_t>(), dnt.as<int32_t>(), 3, nullptr, nullptr, false);
+      EXPECT(pool.status() == 2);  // 2 + 1 of 6 pages fit; the third request needs 4 of the 3 left
+      thrown = false;
+      try { pool.update_batch(FA_PAGE_APPEND, dids.as<int32_t>(), dnt.as<int32_t>(), 3, nullptr, nullptr); }
+      catch (const OutOfPages&) { thrown = true; }
+      EXPECT(thrown);
+      EXPECT(pool.seq_len(2) == 10 && pool.seq_len(0) == 8 && pool.seq_len(1) == 0 && pool.free_pages() == 1);
+    }
     std::printf("paged decode == unpaged; counters score_evals %llu\n",
                 static_cast<unsigned long long>(ctr.score_evals));
   }

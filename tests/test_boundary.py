@@ -36,7 +36,8 @@ def test_ctypes_layout_matches_header(tmp_path):
     structs = {"fa_mask_desc": _lib.MaskDesc, "fa_score_desc": _lib.ScoreDesc,
                "fa_block_mask": _lib.BlockMaskC, "fa_tensor": _lib.TensorC,
                "fa_page_table": _lib.PageTableC, "fa_fwd_args": _lib.FwdArgs,
-               "fa_bwd_args": _lib.BwdArgs, "fa_decode_args": _lib.DecodeArgs}
+               "fa_bwd_args": _lib.BwdArgs, "fa_decode_args": _lib.DecodeArgs,
+               "fa_page_pool": _lib.PagePoolC}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
@@ -60,7 +61,7 @@ def test_status_names():
     lib = _lib.load()
     names = {i: lib.fa_status_name(i).decode() for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 100, 101)}
     assert names[1] == "ShapeMismatch" and names[6] == "BlockMaskMismatch" and names[10] == "UnmappedBlock"
-    assert lib.fa_abi_version() == 3  # v3: flags, counters, phase events, fa_check_finite
+    assert lib.fa_abi_version() == 4  # v3: flags, counters, phase events, fa_check_finite; v4: page pool
 
 
 def test_geometry_validation():

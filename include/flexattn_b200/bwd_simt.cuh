@@ -6,22 +6,17 @@
 //   dk/dv  : warp per kv row over the q-side (transposed) visit list, looping
 //            the kv-batch broadcast and the G query heads of the group (:307-395)
 // Lanes split the head dim; dot products reduce with warp shuffles.
+#pragma once
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
-#include "internal.h"
+#include "host.cuh"
 #include "mods.cuh"
 
 namespace fa {
-
-bool bwd_sm100_supported(const AttnGeom& g);
-fa_status launch_bwd_sm100(const AttnGeom& g, const void* q, const void* k, const void* v,
-                           const void* o, const float* lse, const void* dout, void* dq, void* dk,
-                           void* dv, const BmView& bm, const BmView& bmt, const MaskParams& mp,
-                           int mkind, const ScoreParams& sp, int skind, void* workspace,
-                           const BwdOptions& opt, cudaStream_t st);
-
-namespace {
+namespace bsimt {
+namespace {  // internal linkage: every including translation unit has its own copy
 
 template <typename T>
 __device__ __forceinline__ float ld(const T* p);
@@ -218,51 +213,25 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   return FA_OK;
 }
 
-template <typename T, int MAXP, class ScoreT>
-fa_status by_mask(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
-                  const float* lse, const void* dout, void* dq, void* dk, void* dv,
-                  const BmView& bm, const BmView& bmt, const MaskParams& mp, int mk, ScoreT s,
-                  float* delta, cudaStream_t st) {
-  (void)mk;
-  return run<T, MAXP>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, MaskFn<kMaskDynamic>{mp}, s,
-                      delta, st);
-}
-
-template <typename T, int MAXP>
-fa_status by_score(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
-                   const float* lse, const void* dout, void* dq, void* dk, void* dv,
-                   const BmView& bm, const BmView& bmt, const MaskParams& mp, int mk,
-                   const ScoreParams& sp, int sk, float* delta, cudaStream_t st) {
-  switch (sk) {
-    case 0: return by_mask<T, MAXP>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<0, true>{sp}, delta, st);
-    case 1: return by_mask<T, MAXP>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<1, true>{sp}, delta, st);
-    case 2: return by_mask<T, MAXP>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<2, true>{sp}, delta, st);
-    default: return by_mask<T, MAXP>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mk, ScoreFn<3, true>{sp}, delta, st);
-  }
-}
-
-}  // namespace
-
-fa_status launch_bwd(const AttnGeom& g, const void* q, const void* k, const void* v,
-                     const void* o, const float* lse, const void* dout, void* dq, void* dk,
-                     void* dv, int dtype, const BmView& bm, const BmView& bmt,
-                     const MaskParams& mp, int mkind, const ScoreParams& sp, int skind,
-                     void* workspace, const BwdOptions& opt, cudaStream_t st) {
-  if (dtype == FA_BF16 && bwd_sm100_supported(g))
-    return launch_bwd_sm100(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind,
-                            workspace, opt, st);
-  // the CUDA-core passes are deterministic by construction (separate dq pass, no atomics)
-  // workspace layout (fa_bwd_workspace_size): [dq_acc | delta | lse2]; delta only here
+// The CUDA-core passes for any dtype / head dim <= 128 (deterministic by construction: separate
+// dq pass, no atomics). Workspace layout (fa_bwd_workspace_size): [dq_acc | delta | lse2]; only
+// delta is used here.
+template <class MaskT, class ScoreT>
+fa_status run_any(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
+                  const float* lse, const void* dout, void* dq, void* dk, void* dv, int dtype, const BmView& bm,
+                  const BmView& bmt, MaskT mask, ScoreT score, void* workspace, cudaStream_t st) {
   const size_t rows = (size_t)g.B * g.Hq * g.Lq;
   const size_t off = ((rows * g.D * 4) + 255) & ~size_t(255);
   float* delta = reinterpret_cast<float*>(static_cast<char*>(workspace) + off);
   FA_REQUIRE(g.D <= 128, FA_UNSUPPORTED, "backward: head dim > 128 not compiled");
   if (dtype == FA_F32) {
-    if (g.D <= 32) return by_score<float, 1>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, delta, st);
-    return by_score<float, 4>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, delta, st);
+    if (g.D <= 32) return run<float, 1>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mask, score, delta, st);
+    return run<float, 4>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mask, score, delta, st);
   }
-  if (g.D <= 32) return by_score<__nv_bfloat16, 1>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, delta, st);
-  return by_score<__nv_bfloat16, 4>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mp, mkind, sp, skind, delta, st);
+  if (g.D <= 32) return run<__nv_bfloat16, 1>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mask, score, delta, st);
+  return run<__nv_bfloat16, 4>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt, mask, score, delta, st);
 }
 
+}  // namespace
+}  // namespace bsimt
 }  // namespace fa

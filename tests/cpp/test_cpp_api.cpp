@@ -275,7 +275,11 @@ int main() {
       check_cuda(cudaMemcpy(dids.get(), ids, 12, cudaMemcpyHostToDevice), "ids");
       check_cuda(cudaMemcpy(dnt.get(), nt, 12, cudaMemcpyHostToDevice), "nt");
       pool.update_batch(FA_PAGE_APPEND, dids.as<int32_t>(), dnt.as<int32_t>(), 3, nullptr, nullptr, false);
-      EXPECT(pool.status() == 2);  // 2 + 1 of 6 pages fit; the third request needs 4 of the 3 left
+      // 2 + 1 of 6 pages fit; the third request needs 4 of the 3 left: status() raises it
+      thrown = false;
+      try { pool.status(); } catch (const OutOfPages&) { thrown = true; }
+      EXPECT(thrown);
+      EXPECT(pool.seq_len(2) == 5 && pool.seq_len(0) == 4 && pool.seq_len(1) == 0);
       thrown = false;
       try { pool.update_batch(FA_PAGE_APPEND, dids.as<int32_t>(), dnt.as<int32_t>(), 3, nullptr, nullptr); }
       catch (const OutOfPages&) { thrown = true; }

@@ -266,3 +266,15 @@ def test_paged_decode_mask_range_uses_max_seq_len():
     assert b"flags" in lib.fa_last_error()
     a._pt.max_seq_len = 0  # unknown: the whole logical page range must be covered
     assert lib.fa_flex_decode(C.byref(a), None) == 3
+
+
+def test_user_functor_library_built():
+    """tests/cpp/custom_mods.cu instantiates the kernels with user functors through the public
+    templated header (include/flexattn_b200_device.cuh); build() compiles it for sm_100a."""
+    so = os.path.join(ROOT, "tests", "cpp", "libcustom_mods.so")
+    assert os.path.exists(so), "run __graft_entry__.build()"
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
+    for sym in ("cm_create_block_mask", "cm_forward", "cm_backward", "cm_decode"):
+        assert f" T {sym}" in out
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass  # the tcgen05 / TMA kernels, not a CUDA-core stand-in

@@ -223,10 +223,11 @@ enum {
    * a paged decode that visits a page not owned by the row's batch element
    * (convert_mods, paged_kv.cpp:259-272) -> FA_UNMAPPED_PHYSICAL_INDEX. */
   FA_FLAG_VALIDATE = 1u << 0,
-  /* Backward only: dQ partial sums are added in a fixed order (ascending kv block per q block),
-   * so dq/dk/dv are bitwise reproducible run to run (the reference's worker-count
-   * independence, README.md:104-106). Without it dk/dv are still reproducible but the fp32
-   * dQ additions happen in arrival order. */
+  /* Backward only: the split backward — a dK/dV kernel plus a separate dQ pass that
+   * accumulates each q tile's dQ in TMEM over its kv blocks in one fixed order (the reference's
+   * separate dq pass, engine.cpp:237-305) — so dq/dk/dv are bitwise reproducible run to run (the
+   * reference's worker-count independence, README.md:104-106). Without it dk/dv are still
+   * reproducible but the fused kernel adds fp32 dQ partial sums in arrival order. */
   FA_FLAG_DETERMINISTIC = 1u << 1
 };
 

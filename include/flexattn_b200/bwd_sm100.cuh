@@ -46,6 +46,7 @@
 #include <string>
 #include <type_traits>
 
+#include "bwd_dq.cuh"
 #include "host.cuh"
 #include "mods.cuh"
 #include "sm100_ptx.cuh"
@@ -246,7 +247,18 @@ __device__ __forceinline__ void det_finish_turn(int* turn, int lane) {
   __syncwarp();
 }
 
-template <int D, class MaskT, class ScoreT, bool kDet>
+// kMode: kModeFused (dQ reduce-added by the reduction warps), kModeDet (the same with the adds
+// ordered across kv blocks), kModeNoDQ (dK/dV only; dQ by the separate pass in bwd_dq.cuh)
+enum { kModeFused = 0, kModeDet = 1, kModeNoDQ = 2 };
+#ifndef FA_BWD_SPLIT
+#define FA_BWD_SPLIT 0  // 1: the split (dK/dV kernel + dQ pass) backward by default
+#endif
+constexpr int kDefaultMode = FA_BWD_SPLIT ? kModeNoDQ : kModeFused;
+// FA_FLAG_DETERMINISTIC: the split backward, reproducible by construction (dQ accumulates in
+// TMEM in one fixed kv order; dK/dV per kv block in one fixed q order)
+constexpr int kDeterministicMode = kModeNoDQ;
+
+template <int D, class MaskT, class ScoreT, int kMode>
 __global__ void __launch_bounds__(kThreads, 1)
     flex_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -255,6 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmDQ, const BwdParams p, MaskT mask,
                           ScoreT score) {
   using C = BCfg<D>;
+  constexpr bool kDet = kMode == kModeDet;
+  constexpr bool kNoDQ = kMode == kModeNoDQ;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   BSmem<D>& sm = *reinterpret_cast<BSmem<D>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmDO);
-    if constexpr (C::kTmaReduce) tma_prefetch_desc(&tmDQ);
+    if constexpr (C::kTmaReduce && !kNoDQ) tma_prefetch_desc(&tmDQ);
   }
   if (warp == 13) {
     tmem_alloc(&sm.tmem_base, 512);
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace_ev(p, b, 14);
         mbar_wait(&sm.do_full[ds_], (b / C::kDoStages) & 1);
         trace_ev(p, b, 15);
-        mbar_wait(&sm.dq_empty, (b & 1) ^ 1);
+        if constexpr (!kNoDQ) mbar_wait(&sm.dq_empty, (b & 1) ^ 1);  // dQ^T(b-1) left TMEM
         trace_ev(p, b, 16);
         tc_fence_after();
         mma_kmajor(kDP, v_addr, smem_u32(sm.dO[ds_]), &sm.dp_full);
@@ -449,6 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       };
       auto issue_dq = [&](int b) {  // dQ(b) over the dP columns (dS^T(b) read from smem)
+        if constexpr (kNoDQ) {  // no dQ here: dK(b) only needs dS^T(b) in smem
+          mbar_wait(&sm.ds_full, b & 1);
+          tc_fence_after();
+          return;
+        }
         if constexpr (kDkSS) {
           mbar_wait(&sm.ds_full, b & 1);
           tc_fence_after();
@@ -720,6 +739,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int T = 0, b, h, r;
       bool full;
       while (ti.next(b, h, r, full)) {
+        if constexpr (kNoDQ) {  // the epilogue only needs the task count
+          ++blk;
+          ++T;
+          continue;
+        }
         mbar_wait(&sm.dq_full, blk & 1);
         tc_fence_after();
         if (threadIdx.x == 256) trace_ev(p, blk, 7);
@@ -853,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.dkdv_free);
     }
-    if constexpr (C::kTmaReduce) {
+    if constexpr (C::kTmaReduce && !kNoDQ) {
       if (lane == 0) bulk_wait_group<0>();  // every dQ reduce-add has landed before exit
       __syncwarp();
     }
@@ -912,8 +936,10 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
       a = fmaf(__low2float(xp[e]), __low2float(yp[e]), a);
       a = fmaf(__high2float(xp[e]), __high2float(yp[e]), a);
     }
-    z4[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    z4[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dq_acc != nullptr) {  // the fused dQ reduce-adds into it
+      z4[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z4[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
   if (bad) atomicOr(dout_bad, 1);
   a += __shfl_xor_sync(0xffffffffu, a, 4);
@@ -937,7 +963,7 @@ __global__ void dq_convert_kernel(const float4* __restrict__ acc, uint4* __restr
   }
 }
 
-template <int D, class MaskT, class ScoreT, bool kDet>
+template <int D, class MaskT, class ScoreT, int kMode>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, const void* o,
               const float* lse, const void* dout, void* dq, void* dk, void* dv, const BmView& bm,
               const BmView& bmt, MaskT mask, ScoreT score, void* workspace, const BwdOptions& opt,
@@ -950,7 +976,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
+  constexpr bool kDet = kMode == kModeDet, kNoDQ = kMode == kModeNoDQ;
   int* turn = kDet ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
+  if (kNoDQ) dq_acc = nullptr;  // dQ comes from its own pass: nothing to zero or convert
   if (opt.events[0]) FA_CHECK_CUDA(cudaEventRecord(opt.events[0], st));
   // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
   bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
@@ -959,13 +987,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
-  CUtensorMap mq, mk, mv, mdo, mdq;
+  CUtensorMap mq, mk, mv, mdo, mdq{};
   CUresult cr;
   if ((cr = encode_tile_map(&mq, q, g.B * g.Hq, g.Lq, D)) != CUDA_SUCCESS ||
       (cr = encode_tile_map(&mk, k, g.Bkv * g.Hkv, g.Lkv, D)) != CUDA_SUCCESS ||
       (cr = encode_tile_map(&mv, v, g.Bkv * g.Hkv, g.Lkv, D)) != CUDA_SUCCESS ||
       (cr = encode_tile_map(&mdo, dout, g.B * g.Hq, g.Lq, D)) != CUDA_SUCCESS ||
-      (cr = encode_f32_map(&mdq, dq_acc, g.B * g.Hq, g.Lq, D, BCfg<D>::kBoxD, 32)) != CUDA_SUCCESS)
+      (!kNoDQ && (cr = encode_f32_map(&mdq, dq_acc, g.B * g.Hq, g.Lq, D, BCfg<D>::kBoxD, 32)) != CUDA_SUCCESS))
     return set_error(FA_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")");
   BwdParams p{};
   p.B = g.B; p.Hq = g.Hq; p.Hkv = g.Hkv; p.Bkv = g.Bkv; p.Lq = g.Lq; p.Lkv = g.Lkv; p.G = g.G;
@@ -989,7 +1017,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   }
   p.trace = trace;
   const size_t smem = sizeof(BSmem<D>);
-  auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT, kDet>;
+  auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT, kMode>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
   if (opt.events[1]) FA_CHECK_CUDA(cudaEventRecord(opt.events[1], st));
@@ -1044,8 +1072,15 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
               cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt, acc[5] / cnt,
               acc[6] / cnt, acc[7] / cnt, acc[8] / cnt, acc[9] / cnt, acc[10] / cnt, acc[11] / cnt);
   }
-  const long long n8 = rows * D / 8;
   if (opt.events[2]) FA_CHECK_CUDA(cudaEventRecord(opt.events[2], st));
+  if constexpr (kNoDQ) {
+    // the dQ pass: dQ accumulated in TMEM per q tile, written as bf16
+    const fa_status s = bdq::run<D>(g, q, k, v, dout, lse, delta, dq, bm, mask, score, st);
+    if (s != FA_OK) return s;
+    if (opt.events[3]) FA_CHECK_CUDA(cudaEventRecord(opt.events[3], st));
+    return FA_OK;
+  }
+  const long long n8 = rows * D / 8;
   dq_convert_kernel<<<(unsigned)std::min<long long>((n8 + 255) / 256, 148LL * 16), 256, 0, st>>>(
       reinterpret_cast<const float4*>(dq_acc), static_cast<uint4*>(dq), n8);
   count_launch();

@@ -142,8 +142,8 @@ fa_status flex_bwd_t(const fa_bwd_args* a, MaskT mask, ScoreT score, cudaStream_
 #define FA_BWD_RUN(D, DET)                                                                                       \
   bwd::run<D, MaskT, ScoreT, DET>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->d_out.data, a->dq.data, \
                                   a->dk.data, a->dv.data, bm, bmt, mask, score, a->workspace, opt, st)
-    if (g.D == 128) s = det ? FA_BWD_RUN(128, true) : FA_BWD_RUN(128, false);
-    else s = det ? FA_BWD_RUN(64, true) : FA_BWD_RUN(64, false);
+    if (g.D == 128) s = det ? FA_BWD_RUN(128, bwd::kDeterministicMode) : FA_BWD_RUN(128, bwd::kDefaultMode);
+    else s = det ? FA_BWD_RUN(64, bwd::kDeterministicMode) : FA_BWD_RUN(64, bwd::kDefaultMode);
 #undef FA_BWD_RUN
   } else {
     s = bsimt::run_any(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, a->d_out.data, a->dq.data, a->dk.data,

@@ -64,7 +64,7 @@ inline int num_sms() {
 // kernels and device status flags. The launcher zeroes a word on the stream right before the
 // kernel, so launches on one stream are ordered and launches on different streams never share
 // a word.
-enum { kSlotFwdSched = 0, kSlotBwdSched = 1, kSlotConvertErr = 2, kSlotFiniteErr = 3, kSlotCounters = 4 };
+enum { kSlotFwdSched = 0, kSlotBwdSched = 1, kSlotConvertErr = 2, kSlotFiniteErr = 3, kSlotCounters = 4, kSlotDqSched = 5 };
 inline int* scheduler_counter(int slot, cudaStream_t st) {
   static std::map<std::tuple<int, cudaStream_t, int>, int*> counters;
   static std::mutex mu;

@@ -14,24 +14,24 @@ fa_status by_mask(const AttnGeom& g, const void* q, const void* k, const void* v
                   const BmView& bmt, const MaskParams& mp, int mk, ScoreT s, void* ws,
                   const BwdOptions& opt, cudaStream_t st) {
   // deterministic mode: one instantiation per score kind, the dynamic (any-combination) mask
-  if (opt.flags & FA_FLAG_DETERMINISTIC)
-    return bwd::run<D, MaskFn<kMaskDynamic>, ScoreT, true>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+  if (opt.flags & FA_FLAG_DETERMINISTIC && bwd::kDeterministicMode != bwd::kDefaultMode)
+    return bwd::run<D, MaskFn<kMaskDynamic>, ScoreT, bwd::kDeterministicMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                             MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
   switch (mk) {
     case kMaskNoop:
-      return bwd::run<D, MaskFn<kMaskNoop>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+      return bwd::run<D, MaskFn<kMaskNoop>, ScoreT, bwd::kDefaultMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                             MaskFn<kMaskNoop>{mp}, s, ws, opt, st);
     case kMaskCausalOnly:
-      return bwd::run<D, MaskFn<kMaskCausalOnly>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+      return bwd::run<D, MaskFn<kMaskCausalOnly>, ScoreT, bwd::kDefaultMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                                   MaskFn<kMaskCausalOnly>{mp}, s, ws, opt, st);
     case kMaskSlidingOnly:
-      return bwd::run<D, MaskFn<kMaskSlidingOnly>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+      return bwd::run<D, MaskFn<kMaskSlidingOnly>, ScoreT, bwd::kDefaultMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                                    MaskFn<kMaskSlidingOnly>{mp}, s, ws, opt, st);
     case kMaskDocCausal:
-      return bwd::run<D, MaskFn<kMaskDocCausal>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+      return bwd::run<D, MaskFn<kMaskDocCausal>, ScoreT, bwd::kDefaultMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                                  MaskFn<kMaskDocCausal>{mp}, s, ws, opt, st);
     default:
-      return bwd::run<D, MaskFn<kMaskDynamic>, ScoreT, false>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
+      return bwd::run<D, MaskFn<kMaskDynamic>, ScoreT, bwd::kDefaultMode>(g, q, k, v, o, lse, dout, dq, dk, dv, bm, bmt,
                                                                MaskFn<kMaskDynamic>{mp}, s, ws, opt, st);
   }
 }

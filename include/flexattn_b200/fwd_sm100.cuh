@@ -523,7 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the exponentials run on the FMA pipe (exp2_poly2); measured slower for the others.
         constexpr bool kSplitP = split_p<ScoreT>();
         const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
-        const float nmv = kAlibiTab ? rowc.base - msub : -msub;  // the ALiBi row term rejoins here
+        float nmv = -msub;
+        if constexpr (kAlibiTab) nmv = rowc.base - msub;  // the ALiBi row term rejoins here
         const float2 nm2 = make_float2(nmv, nmv);
         float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};

@@ -277,7 +277,18 @@ def measure_attention(fa, name, c, dev, steps, warmup, seed, stream):
     pre_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ph)
     main_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ph)
     conv_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in ph)
-    del q, k, v, do
+    # the deterministic (split) backward: dK/dV kernel + the TMEM-accumulating dQ pass
+    res = fa.forward(q, k, v, score, bm, cfg)
+    det_ev = timed_events(steps)
+    for i in range(-1, steps):
+        if i >= 0:
+            det_ev[i][0].record(stream)
+        fa.backward(q, k, v, res, do, score, bm, cfg=cfg, deterministic=True)
+        if i >= 0:
+            det_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    det_ms = statistics.mean(a.elapsed_time(b) for a, b in det_ev)
+    del q, k, v, do, res
     fg = c["fwd_gflop"]
     return {"workload": f"{name}: {c['desc']}", "ms_per_step": round(ms, 4),
             "fwd_bwd_tflops": round(3.5 * fg / ms, 2), "fwd_ms": round(fwd_ms, 4),
@@ -286,6 +297,7 @@ def measure_attention(fa, name, c, dev, steps, warmup, seed, stream):
             "bwd_kernels_ms": {"preprocess": round(pre_ms, 4), "main": round(main_ms, 4),
                                "dq_convert": round(conv_ms, 4)},
             "bwd_main_tflops": round(2.5 * fg / main_ms, 2),
+            "bwd_deterministic_ms": round(det_ms, 4), "bwd_deterministic_tflops": round(2.5 * fg / det_ms, 2),
             "fwd_gflop": fg, "block_mask": builder}
 
 

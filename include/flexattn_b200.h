@@ -104,6 +104,10 @@ typedef struct fa_mask_desc {
   int64_t na_width;
   const int32_t* remap;    /* optional device int32[remap_len] slot -> token permutation */
   int64_t remap_len;
+  /* optional (ABI v5), with a remap and FA_MASK_NATTEN as the only term: device
+   * int32[remap_len], (row << 16) | col of token remap[slot] on the na canvas, which replaces
+   * the per-position division of the remapped neighbourhood test (the host layers build it) */
+  const int32_t* remap_rc;
 } fa_mask_desc;
 
 /* ---- score_mod descriptor ---------------------------------------------------

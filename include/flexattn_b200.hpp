@@ -137,6 +137,7 @@ struct MaskMod {
   fa_mask_desc d{};
   std::shared_ptr<void> keep;        // device doc-id table
   std::shared_ptr<void> keep_remap;  // device remap table
+  std::shared_ptr<void> keep_remap_rc;  // device (row, col) table of remapped na_naive
 };
 struct ScoreMod {
   fa_score_desc d{};
@@ -250,6 +251,17 @@ inline MaskMod remap_mask(MaskMod base, const Permutation& p) {
   base.d.remap = buf.as<int32_t>();
   base.d.remap_len = static_cast<i64>(t32.size());
   base.keep_remap = buf.p;
+  if (base.d.terms == FA_MASK_NATTEN && base.d.or_terms == 0 && base.d.na_width > 0 && base.d.na_width < 65536 &&
+      base.d.na_height < 65536) {
+    // (row << 16) | col of every slot's token: the kernels skip the per-position division
+    std::vector<int32_t> rc(t32.size());
+    for (size_t i = 0; i < t32.size(); ++i)
+      rc[i] = static_cast<int32_t>(((t32[i] / base.d.na_width) << 16) | (t32[i] % base.d.na_width));
+    DeviceBuffer rbuf(rc.size() * 4);
+    check_cuda(cudaMemcpy(rbuf.get(), rc.data(), rc.size() * 4, cudaMemcpyHostToDevice), "remap rc table");
+    base.d.remap_rc = rbuf.as<int32_t>();
+    base.keep_remap_rc = rbuf.p;
+  }
   return base;
 }
 

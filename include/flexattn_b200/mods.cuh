@@ -31,6 +31,7 @@ struct MaskParams {
   uint32_t or_terms;       // second AND-group (or_mask)
   int32_t na_w, na_n, na_radius;  // neighbourhood attention canvas (width, tokens, kernel / 2)
   const int32_t* remap;    // slot -> token (remap_mask), or null
+  const int32_t* remap_rc; // slot -> (row << 16) | col of its token (remapped na_naive), or null
 };
 
 struct ScoreParams {
@@ -162,6 +163,54 @@ __device__ __forceinline__ int tile_natten(int a0, int a1, int c0, int c1, int w
   return kTileMixed;
 }
 
+// Remapped na_naive from the slot -> (row << 16 | col) table: the Chebyshev distance of the
+// two tokens' canvas positions (mask_library.cpp:137-149 after remap_mask :203-215).
+__device__ __forceinline__ bool natten_rc(int a, int c, int rad) {
+  return max(abs((a >> 16) - (c >> 16)), abs((a & 0xffff) - (c & 0xffff))) <= rad;
+}
+// bit i = natten_rc(rc[x], rc[y0 + i]) for y0 + i < lim (the other operand fixed)
+__device__ __forceinline__ uint32_t natten_rc_bits32(const int32_t* rc, int x, int y0, int lim, int rad) {
+  const int a = __ldg(rc + x);
+  uint32_t bits = 0;
+  if (y0 + 32 <= lim && (y0 & 3) == 0) {
+    const int4* v = reinterpret_cast<const int4*>(rc + y0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int4 c = __ldg(v + k);
+      bits |= (static_cast<uint32_t>(natten_rc(a, c.x, rad)) | (static_cast<uint32_t>(natten_rc(a, c.y, rad)) << 1) |
+               (static_cast<uint32_t>(natten_rc(a, c.z, rad)) << 2) | (static_cast<uint32_t>(natten_rc(a, c.w, rad)) << 3))
+              << (4 * k);
+    }
+  } else {
+    for (int i = 0; i < 32; ++i)
+      if (y0 + i < lim) bits |= static_cast<uint32_t>(natten_rc(a, __ldg(rc + y0 + i), rad)) << i;
+  }
+  return bits;
+}
+// tile class from the canvas bounding boxes of the tile's q slots [a0, a1] and kv slots
+// [c0, c1] (warp-collective)
+__device__ __forceinline__ int tile_natten_rc(const int32_t* rc, int a0, int a1, int c0, int c1, int rad, int lane) {
+  int qr0 = INT_MAX, qr1 = INT_MIN, qc0 = INT_MAX, qc1 = INT_MIN;
+  int kr0 = INT_MAX, kr1 = INT_MIN, kc0 = INT_MAX, kc1 = INT_MIN;
+  for (int i = a0 + lane; i <= a1; i += 32) {
+    const int v = __ldg(rc + i);
+    qr0 = min(qr0, v >> 16); qr1 = max(qr1, v >> 16); qc0 = min(qc0, v & 0xffff); qc1 = max(qc1, v & 0xffff);
+  }
+  for (int i = c0 + lane; i <= c1; i += 32) {
+    const int v = __ldg(rc + i);
+    kr0 = min(kr0, v >> 16); kr1 = max(kr1, v >> 16); kc0 = min(kc0, v & 0xffff); kc1 = max(kc1, v & 0xffff);
+  }
+  qr0 = __reduce_min_sync(0xffffffffu, qr0); qr1 = __reduce_max_sync(0xffffffffu, qr1);
+  qc0 = __reduce_min_sync(0xffffffffu, qc0); qc1 = __reduce_max_sync(0xffffffffu, qc1);
+  kr0 = __reduce_min_sync(0xffffffffu, kr0); kr1 = __reduce_max_sync(0xffffffffu, kr1);
+  kc0 = __reduce_min_sync(0xffffffffu, kc0); kc1 = __reduce_max_sync(0xffffffffu, kc1);
+  // no pair is within the radius when the boxes are farther apart along rows or columns
+  if (max(qr0 - kr1, kr0 - qr1) > rad || max(qc0 - kc1, kc0 - qc1) > rad) return kTileNone;
+  // every pair is within the radius when the farthest corners are
+  if (max(qr1 - kr0, kr1 - qr0) <= rad && max(qc1 - kc0, kc1 - qc0) <= rad) return kTileAll;
+  return kTileMixed;
+}
+
 template <int K>
 struct MaskFn {
   MaskParams p;
@@ -182,7 +231,8 @@ struct MaskFn {
       if (c == kTileNone) return c;
       return min(c, tile_document(p.doc_ids, a0, a1, c0, c1, lane));
     } else {
-      if (p.remap != nullptr) return kTileMixed;
+      if (p.remap != nullptr)
+        return p.remap_rc != nullptr ? tile_natten_rc(p.remap_rc, a0, a1, c0, c1, p.na_radius, lane) : kTileMixed;
       int g = group_class(p.terms, a0, a1, c0, c1, lane);
       if (p.or_terms != 0u && g != kTileAll) g = max(g, group_class(p.or_terms, a0, a1, c0, c1, lane));
       return g;
@@ -216,6 +266,7 @@ struct MaskFn {
     } else {
       // word-level evaluation of the term groups (one range / vector compare per term); only
       // remapped positions (non-affine) and the per-element terms (natten, hash) fall back
+      if (p.remap_rc != nullptr) return natten_rc_bits32(p.remap_rc, qq, kv0, kv_lim, p.na_radius);
       if (p.remap != nullptr) return mask_bits32_generic(*this, b, h, q, kv0, kv_lim);
       const uint32_t in = range_bits32(kv0, INT_MIN / 2, kv_lim - 1);
       uint32_t bits = group_bits32(p.terms, b, h, qq, kv0, in);
@@ -284,6 +335,8 @@ struct MaskFn {
       if (bits == 0u) return 0u;
       return bits & doc_match_bits32(p.doc_ids, p.doc_len, qq0, __ldg(p.doc_ids + kv));
     } else {
+      if (p.remap_rc != nullptr)  // the window is symmetric: q slots vary at a fixed kv slot
+        return q0 >= q_lim ? 0u : natten_rc_bits32(p.remap_rc, kv, qq0, q_lim + p.q_offset, p.na_radius);
       if (p.remap != nullptr) {
         uint32_t bits = 0;
 #pragma unroll 4
@@ -309,6 +362,7 @@ struct MaskFn {
       // validated on the host before launch (the reference throws IndexOutOfRange).
       return qq >= kv && __ldg(p.doc_ids + qq) == __ldg(p.doc_ids + kv);
     } else {
+      if (p.remap_rc != nullptr) return natten_rc(__ldg(p.remap_rc + qq), __ldg(p.remap_rc + kv), p.na_radius);
       int qs = qq, ks = kv;
       if (p.remap != nullptr) {  // remap_mask, mask_library.cpp:203-215
         qs = __ldg(p.remap + qq);

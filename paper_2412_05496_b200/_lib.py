@@ -21,7 +21,8 @@ class MaskDesc(C.Structure):
                 ("prefix", C.c_int64), ("q_offset", C.c_int64), ("hash_seed", C.c_uint64),
                 ("doc_ids", C.c_void_p), ("doc_len", C.c_int64),
                 ("or_terms", C.c_uint32), ("na_kernel", C.c_int32), ("na_height", C.c_int64),
-                ("na_width", C.c_int64), ("remap", C.c_void_p), ("remap_len", C.c_int64)]
+                ("na_width", C.c_int64), ("remap", C.c_void_p), ("remap_len", C.c_int64),
+                ("remap_rc", C.c_void_p)]
 
 
 class ScoreDesc(C.Structure):

@@ -104,6 +104,12 @@ class MaskMod:
             rm = _device_cache(self, "remap", self.remap, torch.int32, device)
             d.remap = rm.data_ptr()
             d.remap_len = rm.numel()
+            if self.terms == MASK_NATTEN and not self.or_terms and 0 < self.na_width < 65536 \
+                    and self.na_height < 65536:
+                # (row, col) of every slot's token: the kernels skip the per-position division
+                t = torch.as_tensor(self.remap).to(torch.int64)
+                rc = ((t // self.na_width) << 16) | (t % self.na_width)
+                d.remap_rc = _device_cache(self, "remap_rc", rc, torch.int32, device).data_ptr()
         return d
 
 

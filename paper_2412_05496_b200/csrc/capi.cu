@@ -33,6 +33,7 @@ MaskParams to_mask_params(const fa_mask_desc& d) {
   m.na_n = static_cast<int32_t>(d.na_height * d.na_width);
   m.na_radius = d.na_kernel / 2;
   m.remap = d.remap_len > 0 ? d.remap : nullptr;
+  m.remap_rc = (m.remap != nullptr && d.terms == kMaskNatten && d.or_terms == 0) ? d.remap_rc : nullptr;
   return m;
 }
 
@@ -67,6 +68,10 @@ fa_status check_mask_desc(const fa_mask_desc& m, int64_t q_len, int64_t kv_len) 
   if (all & kMaskPrefix)
     FA_REQUIRE(m.prefix >= 0, FA_INDEX_OUT_OF_RANGE, "prefix_lm: prefix_len must be >= 0");
   const int64_t q_end = q_len + m.q_offset;
+  FA_REQUIRE(m.remap_rc == nullptr || m.remap_len > 0, FA_SHAPE_MISMATCH, "remap_mask: remap_rc without a remap");
+  if (m.remap_rc != nullptr)
+    FA_REQUIRE(m.na_width < 65536 && m.na_height < 65536, FA_UNSUPPORTED,
+               "remap_mask: the (row, col) table needs canvas dims < 65536");
   if (m.remap_len > 0) {  // remap_mask range check, mask_library.cpp:208-211
     FA_REQUIRE(m.remap != nullptr, FA_SHAPE_MISMATCH, "remap_mask: table is NULL");
     FA_REQUIRE(m.q_offset >= 0 && q_end <= m.remap_len && kv_len <= m.remap_len, FA_INDEX_OUT_OF_RANGE,
@@ -125,7 +130,7 @@ using namespace capi_detail;
 extern "C" {
 
 const char* fa_last_error(void) { return last_error_ref().c_str(); }
-int32_t fa_abi_version(void) { return 4; }  // v3: flags, counters, phase events, fa_check_finite; v4: device page pool
+int32_t fa_abi_version(void) { return 5; }  // v3: flags, counters, phase events, fa_check_finite; v4: device page pool; v5: remap_rc
 uint64_t fa_launch_count(void) { return launch_counter().load(); }
 
 const char* fa_status_name(fa_status s) {

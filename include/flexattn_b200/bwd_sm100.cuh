@@ -103,6 +103,9 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
 #endif
 constexpr bool kDkSS = FA_BWD_DKSS != 0;
 
+#ifndef FA_BWD_DK_FIRST
+#define FA_BWD_DK_FIRST 0  // 1: issue dK(b) before dQ(b) (frees Q(b) earlier, delays the dQ chain)
+#endif
 #ifndef FA_BWD_DQ_TMA
 #define FA_BWD_DQ_TMA 1
 #endif
@@ -462,15 +465,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
-      auto issue_dq = [&](int b) {  // dQ(b) over the dP columns (dS^T(b) read from smem)
+      auto issue_dq_impl = [&](int b, bool wait) {  // dQ(b) over the dP columns (dS^T(b) read from smem)
         if constexpr (kNoDQ) {  // no dQ here: dK(b) only needs dS^T(b) in smem
-          mbar_wait(&sm.ds_full, b & 1);
-          tc_fence_after();
+          if (wait) {
+            mbar_wait(&sm.ds_full, b & 1);
+            tc_fence_after();
+          }
           return;
         }
         if constexpr (kDkSS) {
-          mbar_wait(&sm.ds_full, b & 1);
-          tc_fence_after();
+          if (wait) {
+            mbar_wait(&sm.ds_full, b & 1);
+            tc_fence_after();
+          }
           trace_ev(p, b, 5);
         }
         trace_ev(p, b, 19);
@@ -493,6 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
+      auto issue_dq = [&](int b) { issue_dq_impl(b, true); };
+      auto issue_dq_nowait = [&](int b) { issue_dq_impl(b, false); };
       auto issue_dk = [&](int b, bool acc) {  // dK += dS^T(b) Q(b)
         if constexpr (kDkSS) {
           // SS, dS^T from the smem buffer (K-major, the layout of a TMA tile): dK is off the
@@ -553,7 +562,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < T; ++t) {
           const int b = blk + t;
           if (t + 1 < T) issue_s(b + 1);
-          if constexpr (kDkSS) {
+          if constexpr (kDkSS && FA_BWD_DK_FIRST != 0) {
+            // dK(b) first: Q(b)'s buffer frees a GEMM earlier for the load of Q(b+2)
+            mbar_wait(&sm.ds_full, b & 1);
+            tc_fence_after();
+            issue_dk(b, t > 0);
+            issue_dq_nowait(b);
+          } else if constexpr (kDkSS) {
             issue_dq(b);
             issue_dk(b, t > 0);
           } else {

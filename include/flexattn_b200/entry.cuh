@@ -13,6 +13,7 @@
 #include "bwd_simt.cuh"
 #include "bwd_sm100.cuh"
 #include "decode.cuh"
+#include "fwd1t.cuh"
 #include "fwd_simt.cuh"
 #include "fwd_sm100.cuh"
 #include "host.cuh"
@@ -60,6 +61,9 @@ fa_status flex_fwd_t(const fa_fwd_args* a, MaskT mask, ScoreT score, cudaStream_
   if (a->q.dtype == FA_BF16 && fwd::supported(g)) {
     s = g.D == 128 ? fwd::run<128>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, bm, mask, score, st)
                    : fwd::run<64>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, bm, mask, score, st);
+  } else if (a->q.dtype == FA_BF16 && fwd1t::supported(g)) {  // rows past the two-tile kernel's list
+    s = g.D == 128 ? fwd1t::run<128>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, bm, mask, score, st)
+                   : fwd1t::run<64>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, bm, mask, score, st);
   } else if (a->q.dtype == FA_F32) {
     s = fsimt::run_any_dim<float>(g, a->q.data, a->k.data, a->v.data, a->out.data, a->lse, bm, mask, score, st);
   } else {

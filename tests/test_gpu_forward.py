@@ -171,3 +171,32 @@ def _slice_check(fa, O, dev, mname, sname, B, Hq, Hkv, L, D, b, h, seed):
 def test_config_slices(fa, O, dev, cfg):
     e_o, e_l = _slice_check(fa, O, dev, *cfg, seed=0x5EED0001)
     assert e_o <= BF16_TOL and e_l <= BF16_TOL, (e_o, e_l)
+
+
+def test_long_rows_take_the_one_tile_kernel(fa, O, dev):
+    """KV_LEN > 131072 (more than 1024 kv blocks per row) runs on the tensor cores through the
+    one-tile kernel, which streams the visit lists from global memory (no CUDA-core fallback)."""
+    B, H, L, D, w = 1, 1, 131072 + 3 * 128 + 77, 64, 200
+    q = fa.random_tensor(91, (B, H, L, D), device=dev)
+    k = fa.random_tensor(92, (B, H, L, D), device=dev)
+    v = fa.random_tensor(93, (B, H, L, D), device=dev)
+    bm = fa.create_block_mask(fa.sliding_window(w), 1, 1, L, L, device=dev)
+    assert bm.cols > 1024
+    res = fa.forward(q, k, v, fa.noop_score(), bm)
+    torch.cuda.synchronize()
+    # check the last 512 rows (the far end of the long rows) against the oracle
+    lo = L - 512
+    om = O.Mask(terms=O.MASK_SLIDING, window=w, q_offset=lo)
+    qf = q[:, :, lo:].float().cpu().numpy()
+    kf, vf = k.float().cpu().numpy(), v.float().cpu().numpy()
+    o_ref, l_ref = O.forward(qf, kf, vf, om, O.Score(), O.create_block_mask(om, 1, 1, 512, L))
+    assert np.abs(res.out[:, :, lo:].float().cpu().numpy() - o_ref).max() <= 2e-2
+    assert np.abs(res.lse[:, :, lo:].cpu().numpy() - l_ref).max() <= 2e-2
+    # the launch is the tensor-core one-tile kernel, not a CUDA-core fallback
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fa.forward(q, k, v, fa.noop_score(), bm)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("flex_fwd1t_kernel" in n for n in names), names
+    assert not any("simt" in n for n in names), names

@@ -12,6 +12,7 @@
 #include "block_mask.cuh"
 #include "bwd_simt.cuh"
 #include "bwd_sm100.cuh"
+#include "dec_tc.cuh"
 #include "decode.cuh"
 #include "fwd1t.cuh"
 #include "fwd_simt.cuh"
@@ -279,7 +280,15 @@ fa_status flex_decode_t(const fa_decode_args* a, const DecodePlan& plan_in, Mask
   if ((s = dec::make_params(plan.g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse, bm, plan.pv,
                             a->workspace, &p)) != FA_OK)
     return s;
-  if ((s = dec::run_any_dim(p, mask, score, st)) != FA_OK) return s;
+  if (dectc::supported(plan.g)) {  // several rows per kv head: one tensor-core tile per (b, kv head)
+    s = plan.g.a.D == 128 ? dectc::run<128>(plan.g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse,
+                                            bm, plan.pv, a->workspace, mask, score, st)
+                          : dectc::run<64>(plan.g, a->q.data, a->k_cache.data, a->v_cache.data, a->out.data, a->lse,
+                                           bm, plan.pv, a->workspace, mask, score, st);
+  } else {
+    s = dec::run_any_dim(p, mask, score, st);
+  }
+  if (s != FA_OK) return s;
   if ((s = end_decode(plan, st)) != FA_OK) return s;
   if (a->counters == nullptr) return FA_OK;
   return compute_counters(plan.g.a, bm, mask, &plan.pv, plan.g.logical_kv, kPassForward, a->counters, st);

@@ -98,3 +98,37 @@ def test_offset_out_of_range(fa, dev):
     bm = fa.create_block_mask(fa.offset_mask(fa.causal(), 255), 1, 1, 1, 256, device=dev)
     with pytest.raises(fa.OffsetOutOfRange):
         fa.decode(q, k, k, 256, fa.causal(), fa.noop_score(), bm)
+
+
+@pytest.mark.parametrize("Hq,Hkv,n_new,L,sname", [(8, 2, 1, 1000, "noop"), (8, 2, 3, 1000, "alibi"),
+                                                  (4, 4, 5, 777, "noop"), (16, 1, 8, 640, "softcap"),
+                                                  (8, 2, 70, 900, "noop")])
+def test_packed_rows_decode_vs_oracle_and_unpaged(fa, O, dev, Hq, Hkv, n_new, L, sname):
+    """GQA groups and multi-token steps (several rows per kv head) take the tensor-core decode,
+    which packs the G heads x n_new rows into one 128-row tile so every page streams once per
+    (batch element, kv head): vs the oracle (decode = forward rows with the offset shift,
+    engine.cpp:403-427), and paged == unpaged bit for bit (acceptance.cpp:312-345)."""
+    B, D = 3, 128
+    off = L - n_new
+    G = Hq // Hkv
+    cache, kl, vl = make_cache(fa, dev, B, Hkv, L, D)
+    q = fa.random_tensor(34, (B, Hq, n_new, D), device=dev)
+    fs, os_ = score_pair(sname, Hq)
+    cfg = fa.AttentionConfig(gqa_group=G)
+    lbm = fa.create_block_mask(fa.offset_mask(fa.causal(), off), 1, 1, n_new, L, device=dev)
+    pt = cache.page_table()
+    pbm = fa.convert_block_mask(lbm, pt)
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        paged = fa.decode(q, cache.k_phys(), cache.v_phys(), off, fa.causal(), fs, pbm, cfg=cfg, page_table=pt)
+        torch.cuda.synchronize()
+    assert any("decode_tc_kernel" in e.name for e in prof.events()), "the tensor-core decode did not run"
+    unpaged = fa.decode(q, kl, vl, off, fa.causal(), fs, lbm, cfg=cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(paged.out, unpaged.out) and torch.equal(paged.lse, unpaged.lse)
+    om = O.causal(off)
+    os_.q_offset = off
+    o_ref, l_ref = O.forward(q.float().cpu().numpy(), kl.float().cpu().numpy(), vl.float().cpu().numpy(),
+                             om, os_, O.create_block_mask(om, 1, 1, n_new, L), gqa=G)
+    assert np.abs(paged.out.float().cpu().numpy() - o_ref).max() <= 2e-2
+    assert lse_err(paged.lse.cpu().numpy(), l_ref) <= 2e-2

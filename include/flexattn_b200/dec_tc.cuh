@@ -32,6 +32,9 @@ namespace fa {
 namespace dectc {
 namespace {  // internal linkage: every including translation unit has its own copy
 
+#ifndef FA_DEC_TC_MIN_ROWS
+#define FA_DEC_TC_MIN_ROWS 2  // rows per kv head from which the tensor-core decode serves a step
+#endif
 constexpr int kThreads = 384;
 constexpr int kTile = 128;
 constexpr float kRescaleThreshold = 8.0f;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 inline bool supported(const DecodeGeom& g) {
   const AttnGeom& a = g.a;
   return (a.D == 128 || a.D == 64) && a.bs_kv == kTile && a.Lq <= kTile && a.rows == 1 &&
-         (a.bm_h == 1 || a.G == 1) && a.G * a.Lq >= 2;
+         (a.bm_h == 1 || a.G == 1) && a.G * a.Lq >= FA_DEC_TC_MIN_ROWS;
 }
 
 template <int D, class MaskT, class ScoreT>

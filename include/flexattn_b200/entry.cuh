@@ -216,8 +216,10 @@ inline fa_status prepare_decode(const fa_decode_args* a, DecodePlan* plan, cudaS
   g.logical_kv = (int)plan->mask_kv;
   int splits = a->num_splits;
   if (splits <= 0) {
+    // the row-per-CTA kernel holds one CTA per SM (192 KB smem): aim for ~28 waves of CTAs
+    // (measured on C5: 2 splits 83.5 % of HBM vs 81.2 % with 1)
     const int64_t rows_total = a->q.b * a->q.h * n_new;
-    const int64_t want = (2LL * num_sms() + rows_total - 1) / rows_total;
+    const int64_t want = (28LL * num_sms() + rows_total - 1) / rows_total;
     splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(64, a->bm->cols)));
   }
   g.num_splits = splits;

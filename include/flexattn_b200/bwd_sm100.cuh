@@ -103,6 +103,12 @@ __device__ __forceinline__ void trace_ev(const BwdParams& p, int task, int ev) {
 #endif
 constexpr bool kDkSS = FA_BWD_DKSS != 0;
 
+#ifndef FA_BWD_REG_REDUCE
+#define FA_BWD_REG_REDUCE 160  // setmaxnreg of the dQ reduction / epilogue warpgroup (128-column drain)
+#endif
+#ifndef FA_BWD_REG_OTHER
+#define FA_BWD_REG_OTHER 64  // setmaxnreg of the producer / MMA warpgroup (160/64: +1..2 %, fewer spills)
+#endif
 #ifndef FA_BWD_DK_FIRST
 #define FA_BWD_DK_FIRST 0  // 1: issue dK(b) before dQ(b) (frees Q(b) earlier, delays the dQ chain)
 #endif
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;                                   \
   } while (0)
   if (warp >= 12) {
-    reg_dealloc<80>();
+    reg_dealloc<FA_BWD_REG_OTHER>();
   }
   if (warp == 12) {
     if (lane == 0) {
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     FA_BWD_TEARDOWN();
   } else if (warp < 12) {
     // ===================== dQ reduction + dK/dV epilogue warpgroup =====================
-    reg_alloc<144>();
+    reg_alloc<FA_BWD_REG_REDUCE>();
     const int wq = warp & 3;
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     int blk = 0, stage_it = 0;

@@ -1,4 +1,4 @@
-// block_mask.cu — BlockMask construction on sm_100a.
+// block_mask.cuh — BlockMask construction on sm_100a.
 //
 // Replaces create_block_mask (block_mask.cpp:79-115), transpose (:161-178) and
 // convert_block_mask (paged_kv.cpp:154-228). Two kernels per build:

@@ -1,4 +1,4 @@
-// bwd_simt.cu — recomputation backward on CUDA cores, the exact-arithmetic
+// bwd_simt.cuh — recomputation backward on CUDA cores, the exact-arithmetic
 // path for fp32 tensors and for geometries the tensor-core backward is not
 // instantiated for. Mirrors backward (engine.cpp:174-401) pass for pass:
 //   delta  : Δ_i = Σ_d dO·O                         (engine.cpp:218-235)

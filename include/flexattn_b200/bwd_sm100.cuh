@@ -1,39 +1,38 @@
-// bwd_sm100.cu — block-sparse FlexAttention backward for sm_100a (bf16 in, fp32
+// bwd_sm100.cuh — block-sparse FlexAttention backward for sm_100a (bf16 in, fp32
 // accumulate), the tensor-core replacement of backward (engine.cpp:174-401).
 //
 // Kernels (one stream, in order):
-//   1. preprocess: Δ_i = Σ_d dO·O (engine.cpp:218-235), stored pre-multiplied by the
-//      softmax scale; lse in log2 units (+inf on fully masked rows so they contribute
-//      exactly nothing, :257-260); both padded to 128-row q blocks.
-//   2. main: persistent, warp-specialised CTA (512 threads). A work item is one
-//      128-row kv block of one (kv batch, kv head) — the dK/dV pass of the
-//      reference (:307-395): it loops the kv-batch broadcast and the G query heads
-//      of the group and walks the transposed (q-side) lists, so dK and dV
-//      accumulate in TMEM for the whole item. Per visited q block t:
+//   1. preprocess: Δ_i = Σ_d dO·O (engine.cpp:218-235) and the compute warps' log2-domain
+//      column term log2(scale) - lse·log2e (-inf on fully masked rows so they contribute
+//      exactly nothing, :257-260), both padded to 128-row q blocks; zeroes the fp32 dQ
+//      accumulator (fused mode).
+//   2. main: persistent, warp-specialised CTA (512 threads; setmaxnreg 144 compute / 160 dQ
+//      reduction / 64 producer+MMA). A work item is one 128-row kv block of one (kv batch,
+//      kv head) — the dK/dV pass of the reference (:307-395): it loops the kv-batch broadcast
+//      and the G query heads of the group and walks the transposed (q-side) lists, so dK and
+//      dV accumulate in TMEM for the whole item. Per visited q block t:
 //        S^T  = K Q^T          (SS)             -> TMEM S    [0,128)
 //        dP^T = V dO^T         (SS)             -> TMEM dP   [128,256)
-//        compute warps, phase A (after S^T):  (P·scale)^T = exp2(score_mod(S^T) - lse + log2
-//           scale), mask_mod only in partial blocks, as bf16 into TMEM over S^T (dV is rescaled
-//           by 1/scale in the epilogue); P·scale·mod' kept in registers as packed bf16
-//        compute warps, phase B (after dP^T): dS^T = P (dP^T - Δ) mod' scale (bf16) into
-//           TMEM over dP^T and into smem
+//        compute warps, phase A (after S^T): (P·scale)^T = exp2(s·c + cterm), mask_mod only
+//           in partial blocks, as bf16 into TMEM over S^T (dV is rescaled by 1/scale in the
+//           epilogue); P·scale·mod' kept in registers (fp32)
+//        compute warps, phase B (after dP^T): dS^T = P (dP^T - Δ) mod' scale (bf16) into the
+//           smem dS^T buffer
 //        dV  += P^T dO          (TS: P^T from TMEM)
-//        dK  += dS^T Q          (TS: dS^T from TMEM)
+//        dK  += dS^T Q          (SS: dS^T from the smem buffer)
 //        dQ^T = K^T dS^T        (SS, both MN-major) -> TMEM over the dP columns
 //      The MMA warp software-pipelines consecutive blocks so the tensor core runs the
 //      GEMMs of one block while the compute warps work on the next:
 //          S(t+1) | dQ(t) | dK(t) | dP(t+1) | dV(t+1) | S(t+2) | ...
-//      Shared memory bandwidth (128 B/clk/SM) is the scarce resource: an SS 128x128x16
-//      MMA alone reads 128 B/clk, so dV (P^T already in TMEM) is TS; dK reads dS^T from
-//      the same smem buffer as dQ. dQ (the fused form of the reference's separate dQ
-//      pass, :237-305) is drained from TMEM by the reduction warpgroup into per-warp
-//      32x32 fp32 smem tiles and added into the fp32 accumulator in L2 with TMA
-//      cp.reduce.async.bulk.tensor (add). The order of those adds across kv blocks is
-//      not fixed, so dQ is not bitwise reproducible run to run unless the deterministic
-//      mode orders them (see FA_BWD_DETERMINISTIC below).
+//      dQ (the fused form of the reference's separate dQ pass, :237-305) is drained from
+//      TMEM by the reduction warpgroup into per-warp 32x32 fp32 smem tiles and added into
+//      the fp32 accumulator in L2 with TMA cp.reduce.async.bulk.tensor (add). The order of
+//      those adds across kv blocks is not fixed, so the fused dQ is not bitwise reproducible
+//      run to run; FA_FLAG_DETERMINISTIC runs the split backward instead (kModeNoDQ here,
+//      dK/dV only, plus the dQ pass of bwd_dq.cuh).
 //      Warps 0-7 compute (two warpgroups, 64 q columns each; thread = kv row),
 //      warps 8-11 dQ reduction + dK/dV epilogue, warp 12 TMA producer, warp 13 MMA.
-//   3. convert: dQ fp32 -> bf16.
+//   3. convert: dQ fp32 -> bf16 (fused mode).
 #pragma once
 
 #include <cuda.h>

@@ -1,4 +1,4 @@
-// decode.cu — split-KV (paged) decode for short query steps, the HBM-bound
+// decode.cuh — split-KV (paged) decode for short query steps, the HBM-bound
 // replacement of decode (engine.cpp:403-427) composed with the paged-KV index
 // rewrite (convert_block_mask, paged_kv.cpp:154-228) and the logical-position
 // recovery of convert_mods (paged_kv.cpp:230-310).

@@ -1,4 +1,4 @@
-// fwd_simt.cu — exact-arithmetic (fp32 FFMA) block-sparse forward.
+// fwd_simt.cuh — exact-arithmetic (fp32 FFMA) block-sparse forward.
 //
 // Serves the fp32 configuration (BASELINE config C1, gate 1e-4 vs the
 // reference forward<float>) and every geometry the tensor-core kernel is not

@@ -1,4 +1,4 @@
-// fwd_sm100.cu — block-sparse FlexAttention forward for sm_100a (bf16 in,
+// fwd_sm100.cuh — block-sparse FlexAttention forward for sm_100a (bf16 in,
 // fp32 accumulate), the tensor-core replacement of forward_impl
 // (engine.cpp:46-163).
 //

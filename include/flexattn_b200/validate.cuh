@@ -1,4 +1,4 @@
-// validate.cu — data-dependent checks and work counters of the reference, on the device.
+// validate.cuh — data-dependent checks and work counters of the reference, on the device.
 //
 //  * finite_scan_kernel: the NaN/inf scans of validate_inputs (validate.hpp:36-38) and of the
 //    backward's d_out (engine.cpp:196), several tensors in one grid-stride pass with 16-byte

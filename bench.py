@@ -344,11 +344,33 @@ def measure_decode(fa, dev, steps, warmup, stream, hbm):
             "l2": "34.4 GB of K/V per step >> 126 MB L2 (no flush needed)"}
 
 
+def bind_to_gpu_numa(local):
+    """Pin this process to the CPUs of the GPU's NUMA node (sysfs local_cpulist), so the pinned
+    host buffers of the e2e leg live next to the GPU's PCIe root; returns the previous mask."""
+    import torch
+    prev = os.sched_getaffinity(0)
+    try:
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        if cpus and cpus != prev:
+            os.sched_setaffinity(0, cpus)
+    except Exception:  # no sysfs entry / attribute: leave the mask as it is
+        pass
+    return prev
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cpu_mask = bind_to_gpu_numa(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
@@ -552,6 +574,7 @@ def run_ours(args):
         line["configs"] = per_config
     if world == 1 and not args.no_cpu_baseline:
         try:
+            os.sched_setaffinity(0, cpu_mask)  # the CPU reference gets every host core again
             cb = cpu_reference_sample(c)
             line["cpu_baseline"] = {
                 "value": round(cb["gflop"] / cb["seconds"] / 1000.0, 6), "unit": "TFLOP/s",

@@ -12,3 +12,9 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --headline-only --no-cpu-baseline > /dev/null 2>&1
 timeout 900 bash tools/ncu_capture.sh C2 ${TAG}
+# summarise the captures on the box (the .ncu-rep files would overflow the 64 MiB copy-back)
+for k in fwd bwd; do
+  [ -f gpurun_out/ncu_${k}_C2_${TAG}.ncu-rep ] && python tools/ncu_summary.py gpurun_out/ncu_${k}_C2_${TAG}.ncu-rep > gpurun_out/${TAG}_${k}_c2_ncu.txt 2>&1
+  ncu -i gpurun_out/ncu_${k}_C2_${TAG}.ncu-rep --page raw --csv > gpurun_out/${TAG}_${k}_c2_raw.csv 2>/dev/null
+done
+rm -f gpurun_out/*.ncu-rep

@@ -1,11 +1,13 @@
 """Paged split-KV decode on the GPU: vs the oracle (decode = forward rows with the offset shift,
 engine.cpp:403-427), paged == unpaged bit for bit (acceptance.cpp:312-345 contract), and the
 page-converted BlockMask bit-exact vs convert_block_mask (paged_kv.cpp:154-228)."""
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
 
-from helpers import lse_err, score_pair
+from helpers import lse_err, mask_pair, score_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -100,10 +102,14 @@ def test_offset_out_of_range(fa, dev):
         fa.decode(q, k, k, 256, fa.causal(), fa.noop_score(), bm)
 
 
-@pytest.mark.parametrize("Hq,Hkv,n_new,L,sname", [(8, 2, 1, 1000, "noop"), (8, 2, 3, 1000, "alibi"),
-                                                  (4, 4, 5, 777, "noop"), (16, 1, 8, 640, "softcap"),
-                                                  (8, 2, 70, 900, "noop")])
-def test_packed_rows_decode_vs_oracle_and_unpaged(fa, O, dev, Hq, Hkv, n_new, L, sname):
+@pytest.mark.parametrize("Hq,Hkv,n_new,L,sname,mname", [(8, 2, 1, 1000, "noop", "causal"),
+                                                        (8, 2, 3, 1000, "alibi", "causal"),
+                                                        (4, 4, 5, 777, "noop", "causal"),
+                                                        (16, 1, 8, 640, "softcap", "causal"),
+                                                        (8, 2, 70, 900, "noop", "causal"),
+                                                        (8, 2, 4, 1000, "alibi", "sliding:300"),
+                                                        (4, 1, 6, 850, "stacked", "sliding:130")])
+def test_packed_rows_decode_vs_oracle_and_unpaged(fa, O, dev, Hq, Hkv, n_new, L, sname, mname):
     """GQA groups and multi-token steps (several rows per kv head) take the tensor-core decode,
     which packs the G heads x n_new rows into one 128-row tile so every page streams once per
     (batch element, kv head): vs the oracle (decode = forward rows with the offset shift,
@@ -115,18 +121,19 @@ def test_packed_rows_decode_vs_oracle_and_unpaged(fa, O, dev, Hq, Hkv, n_new, L,
     q = fa.random_tensor(34, (B, Hq, n_new, D), device=dev)
     fs, os_ = score_pair(sname, Hq)
     cfg = fa.AttentionConfig(gqa_group=G)
-    lbm = fa.create_block_mask(fa.offset_mask(fa.causal(), off), 1, 1, n_new, L, device=dev)
+    fm, om = mask_pair(mname, L)
+    lbm = fa.create_block_mask(fa.offset_mask(fm, off), 1, 1, n_new, L, device=dev)
     pt = cache.page_table()
     pbm = fa.convert_block_mask(lbm, pt)
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        paged = fa.decode(q, cache.k_phys(), cache.v_phys(), off, fa.causal(), fs, pbm, cfg=cfg, page_table=pt)
+        paged = fa.decode(q, cache.k_phys(), cache.v_phys(), off, fm, fs, pbm, cfg=cfg, page_table=pt)
         torch.cuda.synchronize()
     assert any("decode_tc_kernel" in e.name for e in prof.events()), "the tensor-core decode did not run"
-    unpaged = fa.decode(q, kl, vl, off, fa.causal(), fs, lbm, cfg=cfg)
+    unpaged = fa.decode(q, kl, vl, off, fm, fs, lbm, cfg=cfg)
     torch.cuda.synchronize()
     assert torch.equal(paged.out, unpaged.out) and torch.equal(paged.lse, unpaged.lse)
-    om = O.causal(off)
+    om = dataclasses.replace(om, q_offset=off)
     os_.q_offset = off
     o_ref, l_ref = O.forward(q.float().cpu().numpy(), kl.float().cpu().numpy(), vl.float().cpu().numpy(),
                              om, os_, O.create_block_mask(om, 1, 1, n_new, L), gqa=G)

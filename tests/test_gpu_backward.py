@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_bwd(fa, O, dev, mname, sname, B=1, Hq=2, Hkv=2, Lq=384, Lkv=384, D=128, bs=128,
-            dtype=torch.bfloat16, Bkv=None, seed=300, mask_dims=(1, 1)):
+            dtype=torch.bfloat16, Bkv=None, seed=300, mask_dims=(1, 1), deterministic=False):
     Bkv = B if Bkv is None else Bkv
     fm, om = mask_pair(mname, max(Lq, Lkv))
     fs, os_ = score_pair(sname, Hq)
@@ -24,7 +24,7 @@ def run_bwd(fa, O, dev, mname, sname, B=1, Hq=2, Hkv=2, Lq=384, Lkv=384, D=128, 
     bm = fa.create_block_mask(fm, mask_dims[0], mask_dims[1], Lq, Lkv, bs, bs, device=dev)
     cfg = fa.AttentionConfig(gqa_group=Hq // Hkv, block_size_q=bs, block_size_kv=bs)
     fwd = fa.forward(q, k, v, fs, bm, cfg)
-    g = fa.backward(q, k, v, fwd, do, fs, bm, cfg=cfg)
+    g = fa.backward(q, k, v, fwd, do, fs, bm, cfg=cfg, deterministic=deterministic)
     torch.cuda.synchronize()
     qf, kf, vf, dof = (x.float().cpu().numpy() for x in (q, k, v, do))
     obm = O.create_block_mask(om, mask_dims[0], mask_dims[1], Lq, Lkv, bs, bs)
@@ -54,6 +54,22 @@ def test_bwd_shapes(fa, O, dev, D, shape):
 def test_bwd_gqa_broadcast(fa, O, dev):
     # shared kv batch + GQA group loop (engine.cpp:326-331)
     errs = run_bwd(fa, O, dev, "causal", "alibi", B=2, Hq=4, Hkv=1, Bkv=1, Lq=256, Lkv=256)
+    assert max(errs) <= 2e-2, errs
+
+
+@pytest.mark.parametrize("mname", ["noop", "causal", "sliding:200", "doc_causal", "hash:909:200"])
+@pytest.mark.parametrize("sname", ["noop", "alibi", "softcap:20"])
+def test_bwd_deterministic_masks_scores(fa, O, dev, mname, sname):
+    # the split backward (dK/dV-only kernel + the TMEM-accumulating dQ pass, bwd_dq.cuh)
+    errs = run_bwd(fa, O, dev, mname, sname, deterministic=True)
+    assert max(errs) <= 2e-2, errs
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_bwd_deterministic_shapes_gqa(fa, O, dev, D):
+    errs = run_bwd(fa, O, dev, "causal", "alibi", B=2, Hq=4, Hkv=2, Bkv=1, Lq=500, Lkv=500, D=D, deterministic=True)
+    assert max(errs) <= 2e-2, errs
+    errs = run_bwd(fa, O, dev, "noop", "noop", Lq=300, Lkv=700, D=D, deterministic=True)
     assert max(errs) <= 2e-2, errs
 
 

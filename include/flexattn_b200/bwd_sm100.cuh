@@ -108,6 +108,9 @@ constexpr bool kDkSS = FA_BWD_DKSS != 0;
 #ifndef FA_BWD_REG_OTHER
 #define FA_BWD_REG_OTHER 64  // setmaxnreg of the producer / MMA warpgroup (160/64: +1..2 %, fewer spills)
 #endif
+#ifndef FA_BWD_L2PF
+#define FA_BWD_L2PF 0  // 1: L2 prefetch of the next task's Q / dO tiles (one task ahead)
+#endif
 #ifndef FA_BWD_DK_FIRST
 #define FA_BWD_DK_FIRST 0  // 1: issue dK(b) before dQ(b) (frees Q(b) earlier, delays the dQ chain)
 #endif
@@ -368,7 +371,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         int b, h, r;
         bool full;
         bool v_loaded = false;
-        while (ti.next(b, h, r, full)) {
+        // one task of lookahead: the next q block's Q / dO tiles are prefetched into L2 while
+        // this one's buffers are still busy (FA_BWD_L2PF)
+        int nb_ = 0, nh_ = 0, nr_ = 0;
+        bool nfull_ = false;
+        bool have = ti.next(nb_, nh_, nr_, nfull_);
+        while (have) {
+          b = nb_;
+          h = nh_;
+          r = nr_;
+          full = nfull_;
+          have = ti.next(nb_, nh_, nr_, nfull_);
+          if (FA_BWD_L2PF != 0 && have) {
+            for (int ch = 0; ch < C::kChunks; ++ch) {
+              tma_prefetch_l2_3d(&tmQ, ch * 64, nr_ * kTile, nb_ * p.Hq + nh_);
+              tma_prefetch_l2_3d(&tmDO, ch * 64, nr_ * kTile, nb_ * p.Hq + nh_);
+            }
+          }
           const int st = blk & 1;
           const long long row0 = static_cast<long long>(b * p.Hq + h) * p.Lq_pad + r * kTile;
           mbar_wait(&sm.q_free[st], ((blk >> 1) & 1) ^ 1);

@@ -201,6 +201,11 @@ FA_API fa_status fa_transpose_block_mask(fa_block_mask* bm, void* workspace, siz
  * reported with FA_UNMAPPED_BLOCK after the stream is synchronised by the call. */
 FA_API fa_status fa_convert_block_mask(const fa_block_mask* logical, const fa_page_table* pt,
                                 fa_block_mask* out, void* stream);
+/* The same without a host round trip (ABI v6): the device int32 *status is zeroed and then set
+ * to 1 when a referenced logical block has no physical page (the caller checks it when it
+ * synchronises anyway), so a serving step can be captured in a CUDA graph. */
+FA_API fa_status fa_convert_block_mask_async(const fa_block_mask* logical, const fa_page_table* pt,
+                                             fa_block_mask* out, int32_t* status, void* stream);
 
 /* ---- attention ---------------------------------------------------------------- */
 /* Work counters of the reference (OpCounters, engine.hpp:21-32), computed on the device from the

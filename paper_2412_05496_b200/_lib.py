@@ -100,7 +100,7 @@ EXPORTS = [
     "fa_convert_block_mask", "fa_flex_fwd", "fa_bwd_workspace_size", "fa_flex_bwd",
     "fa_decode_workspace_size", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
     "fa_check_finite", "fa_page_pool_bytes", "fa_page_pool_init", "fa_page_pool_shuffle",
-    "fa_page_pool_update", "fa_page_pool_status", "fa_page_pool_table",
+    "fa_page_pool_update", "fa_page_pool_status", "fa_page_pool_table", "fa_convert_block_mask_async",
 ]
 
 _lib = None
@@ -128,6 +128,8 @@ def load():
     lib.fa_transpose_block_mask.argtypes = [C.POINTER(BlockMaskC), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.fa_convert_block_mask.argtypes = [C.POINTER(BlockMaskC), C.POINTER(PageTableC),
                                           C.POINTER(BlockMaskC), C.c_void_p]
+    lib.fa_convert_block_mask_async.argtypes = [C.POINTER(BlockMaskC), C.POINTER(PageTableC),
+                                                C.POINTER(BlockMaskC), C.c_void_p, C.c_void_p]
     lib.fa_flex_fwd.argtypes = [C.POINTER(FwdArgs), C.c_void_p]
     lib.fa_bwd_workspace_size.restype = C.c_size_t
     lib.fa_bwd_workspace_size.argtypes = [C.c_int64] * 4
@@ -150,7 +152,7 @@ def load():
     lib.fa_page_pool_status.argtypes = [C.POINTER(PagePoolC), C.POINTER(C.c_int32), C.c_void_p]
     lib.fa_page_pool_table.restype = PageTableC
     lib.fa_page_pool_table.argtypes = [C.POINTER(PagePoolC)]
-    for fn in ("fa_page_pool_init", "fa_page_pool_shuffle", "fa_page_pool_update", "fa_page_pool_status",
+    for fn in ("fa_convert_block_mask_async", "fa_page_pool_init", "fa_page_pool_shuffle", "fa_page_pool_update", "fa_page_pool_status",
                "fa_create_block_mask", "fa_transpose_block_mask", "fa_convert_block_mask",
                "fa_flex_fwd", "fa_flex_bwd", "fa_flex_decode", "fa_fill_uniform", "fa_paged_write",
                "fa_block_mask_geometry", "fa_check_finite"):

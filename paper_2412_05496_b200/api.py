@@ -779,8 +779,9 @@ class DevicePageTable:
     """Live view of a device page pool as a PageTable (paged_kv.hpp:18-41): the kernels read the
     pool's own arrays (no upload); the host lists are downloaded on access."""
 
-    def __init__(self, cache: "PagedKVCache"):
+    def __init__(self, cache: "PagedKVCache", max_seq_len: Optional[int] = None):
         self._cache = cache
+        self._max_seq_len = max_seq_len
         self.batches = cache.batches
         self.max_logical_pages = cache.num_pages
         self.num_physical_pages = cache.num_pages
@@ -810,7 +811,7 @@ class DevicePageTable:
 
     def c(self, device=None) -> PageTableC:
         s = _lib.load().fa_page_pool_table(C.byref(self._cache._pool))
-        s.max_seq_len = self._cache._max_seq_len()
+        s.max_seq_len = self._max_seq_len if self._max_seq_len is not None else self._cache._max_seq_len()
         return s
 
 
@@ -858,8 +859,11 @@ class PagedKVCache:
             self._host_valid = True
         return max(self._seq_host) if self._seq_host else 0
 
-    def page_table(self) -> DevicePageTable:
-        return DevicePageTable(self)
+    def page_table(self, max_seq_len: Optional[int] = None) -> DevicePageTable:
+        """The live device page table. ``max_seq_len`` (an upper bound of the sequence lengths,
+        for the mask's range checks) avoids reading the lengths back after ``sync=False``
+        updates."""
+        return DevicePageTable(self, max_seq_len)
 
     def shuffle_free_pages(self, seed: int):
         """shuffle_free_pages (paged_kv.cpp:143-146) of the device free stack."""
@@ -971,20 +975,33 @@ class PagedKVCache:
         return self.num_pages * self.ps
 
 
-def convert_block_mask(bm: BlockMask, pt: PageTable) -> BlockMask:
-    """convert_block_mask (paged_kv.cpp:154-228) on the GPU: logical block columns -> pages."""
+def convert_block_mask(bm: BlockMask, pt: PageTable, out: Optional[BlockMask] = None,
+                       status: Optional[torch.Tensor] = None) -> BlockMask:
+    """convert_block_mask (paged_kv.cpp:154-228) on the GPU: logical block columns -> pages.
+    ``out`` reuses a converted mask of the same geometry; with a device int32 ``status`` tensor
+    the call does not synchronise (UnmappedBlock is reported as status[0] == 1 instead), so a
+    serving step can be captured in a CUDA graph."""
     dev = bm.device
     i32 = dict(dtype=torch.int32, device=dev)
     rows, cols = bm.rows, pt.num_physical_pages
     n = pt.batches * bm.h_dims
-    out = BlockMask(pt.batches, bm.h_dims, rows, cols, bm.bs_q, bm.bs_kv, bm.q_len,
-                    pt.num_physical_pages * pt.page_size, torch.empty(n * rows, **i32),
-                    torch.empty(n * rows * cols, **i32), torch.empty(n * rows, **i32),
-                    torch.empty(n * rows * cols, **i32), mask=bm.mask)
+    if out is None:
+        out = BlockMask(pt.batches, bm.h_dims, rows, cols, bm.bs_q, bm.bs_kv, bm.q_len,
+                        pt.num_physical_pages * pt.page_size, torch.empty(n * rows, **i32),
+                        torch.empty(n * rows * cols, **i32), torch.empty(n * rows, **i32),
+                        torch.empty(n * rows * cols, **i32), mask=bm.mask)
+    elif out.kv_indices.numel() != n * rows * cols or out.kv_num_blocks.numel() != n * rows:
+        raise BlockMaskMismatch("convert_block_mask: `out` has another geometry")
     cl, co = bm.c(), out.c()
     cpt = pt.c(dev)
-    _check(_lib.load().fa_convert_block_mask(C.byref(cl), C.byref(cpt), C.byref(co),
-                                             C.c_void_p(_stream())))
+    lib = _lib.load()
+    if status is None:
+        _check(lib.fa_convert_block_mask(C.byref(cl), C.byref(cpt), C.byref(co), C.c_void_p(_stream())))
+    else:
+        if status.dtype != torch.int32 or not status.is_cuda:
+            raise ShapeMismatch("convert_block_mask: status must be a device int32 tensor")
+        _check(lib.fa_convert_block_mask_async(C.byref(cl), C.byref(cpt), C.byref(co),
+                                               C.c_void_p(status.data_ptr()), C.c_void_p(_stream())))
     return out
 
 

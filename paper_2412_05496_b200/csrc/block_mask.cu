@@ -62,15 +62,18 @@ extern "C" fa_status fa_transpose_block_mask(fa_block_mask* bm, void* workspace,
   return FA_OK;
 }
 
-extern "C" fa_status fa_convert_block_mask(const fa_block_mask* lg, const fa_page_table* pt,
-                                           fa_block_mask* out, void* stream) {
-  clear_error();
+namespace {
+
+// convert_block_mask's geometry checks and kernel; unmapped blocks set *d_err (stream-ordered)
+fa_status convert_launch(const fa_block_mask* lg, const fa_page_table* pt, fa_block_mask* out, int* d_err,
+                         cudaStream_t st) {
   FA_REQUIRE(lg && pt && out, FA_SHAPE_MISMATCH, "convert_block_mask: NULL argument");
   FA_REQUIRE(lg->bs_kv == pt->page_size, FA_BLOCK_MASK_MISMATCH,
              "convert_block_mask: kv block size " + std::to_string(lg->bs_kv) +
                  " must equal page size " + std::to_string(pt->page_size));
   FA_REQUIRE(lg->b_dims == 1 || lg->b_dims == pt->batches, FA_BLOCK_MASK_MISMATCH,
              "convert_block_mask: mask batch dim must be 1 or " + std::to_string(pt->batches));
+  FA_REQUIRE(d_err != nullptr, FA_CUDA_ERROR, "convert_block_mask: no status word");
   out->b_dims = pt->batches;
   out->h_dims = lg->h_dims;
   out->rows = lg->rows;
@@ -79,9 +82,6 @@ extern "C" fa_status fa_convert_block_mask(const fa_block_mask* lg, const fa_pag
   out->bs_kv = lg->bs_kv;
   out->q_len = lg->q_len;
   out->kv_len = pt->num_physical_pages * pt->page_size;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int* d_err = scheduler_counter(kSlotConvertErr, st);  // this (device, stream)'s status word
-  FA_REQUIRE(d_err != nullptr, FA_CUDA_ERROR, "convert_block_mask: cannot allocate the status word");
   FA_CHECK_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), st));
   const int nlines = (int)(out->b_dims * out->h_dims * out->rows);
   bmk::convert_kernel<<<nlines, 128, 0, st>>>((int)pt->batches, (int)lg->h_dims, (int)lg->rows,
@@ -92,10 +92,29 @@ extern "C" fa_status fa_convert_block_mask(const fa_block_mask* lg, const fa_pag
                                          out->full_kv_num_blocks, out->full_kv_indices, d_err);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
+  return FA_OK;
+}
+
+}  // namespace
+
+extern "C" fa_status fa_convert_block_mask(const fa_block_mask* lg, const fa_page_table* pt,
+                                           fa_block_mask* out, void* stream) {
+  clear_error();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* d_err = scheduler_counter(kSlotConvertErr, st);  // this (device, stream)'s status word
+  fa_status s = convert_launch(lg, pt, out, d_err, st);
+  if (s != FA_OK) return s;
   int h_err = 0;
   FA_CHECK_CUDA(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FA_CHECK_CUDA(cudaStreamSynchronize(st));
   FA_REQUIRE(h_err == 0, FA_UNMAPPED_BLOCK,
              "convert_block_mask: a logical block referenced by the mask has no physical page");
   return FA_OK;
+}
+
+extern "C" fa_status fa_convert_block_mask_async(const fa_block_mask* lg, const fa_page_table* pt,
+                                                 fa_block_mask* out, int32_t* status, void* stream) {
+  clear_error();
+  FA_REQUIRE(status != nullptr, FA_SHAPE_MISMATCH, "convert_block_mask_async: NULL status word");
+  return convert_launch(lg, pt, out, status, static_cast<cudaStream_t>(stream));
 }

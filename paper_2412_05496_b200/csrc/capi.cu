@@ -130,7 +130,7 @@ using namespace capi_detail;
 extern "C" {
 
 const char* fa_last_error(void) { return last_error_ref().c_str(); }
-int32_t fa_abi_version(void) { return 5; }  // v3: flags, counters, phase events, fa_check_finite; v4: device page pool; v5: remap_rc
+int32_t fa_abi_version(void) { return 6; }  // v3: flags, counters, phase events, fa_check_finite; v4: device page pool; v5: remap_rc; v6: async convert
 uint64_t fa_launch_count(void) { return launch_counter().load(); }
 
 const char* fa_status_name(fa_status s) {

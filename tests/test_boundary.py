@@ -61,7 +61,7 @@ def test_status_names():
     lib = _lib.load()
     names = {i: lib.fa_status_name(i).decode() for i in (0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 100, 101)}
     assert names[1] == "ShapeMismatch" and names[6] == "BlockMaskMismatch" and names[10] == "UnmappedBlock"
-    assert lib.fa_abi_version() == 5  # v3: flags, counters, phase events, fa_check_finite; v4: page pool; v5: remap_rc
+    assert lib.fa_abi_version() == 6  # v3 flags/counters/events/check_finite; v4 page pool; v5 remap_rc; v6 async convert
 
 
 def test_geometry_validation():

@@ -301,6 +301,28 @@ def measure_attention(fa, name, c, dev, steps, warmup, seed, stream):
             "fwd_gflop": fg, "block_mask": builder}
 
 
+def measure_c1(fa, dev, steps, stream):
+    """C1: causal B1 H4 S1024 D64 fp32 forward (the reference's CPU-runnable case) on the
+    exact-arithmetic CUDA-core kernel (1e-4 gate); 0.537 GFLOP of live pairs."""
+    import torch
+    B, H, L, D = 1, 4, 1024, 64
+    q, k, v = (fa.random_tensor(SEED + i, (B, H, L, D), dtype=torch.float32, device=dev) for i in (1, 2, 3))
+    bm = fa.create_block_mask(fa.causal(), 1, 1, L, L, device=dev)
+    for _ in range(3):
+        fa.forward(q, k, v, fa.noop_score(), bm)
+    torch.cuda.synchronize()
+    ev = timed_events(steps)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        fa.forward(q, k, v, fa.noop_score(), bm)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    gflop = 4 * D * B * H * (L * (L + 1) // 2) / 1e9
+    return {"workload": "C1: causal B1 H4 S1024 D64 fp32 forward (CUDA-core exact path)", "ms": round(ms, 4),
+            "tflops": round(gflop / ms, 3), "gflop": round(gflop, 4)}
+
+
 def measure_decode(fa, dev, steps, warmup, stream, hbm):
     """C5: paged split-KV decode, HBM-bound (bytes = K + V of every visited page)."""
     import torch
@@ -528,6 +550,7 @@ def run_ours(args):
                                                  max(3, args.warmup), SEED, stream)
             per_config[name]["pct_of_peak_fwd_bwd"] = round(100 * per_config[name]["fwd_bwd_tflops"] / peak, 2)
             torch.cuda.empty_cache()
+        per_config["C1"] = measure_c1(fa, dev, max(5, min(steps, 20)), stream)
         try:
             per_config["C5"] = measure_decode(fa, dev, max(5, min(steps, 20)), max(3, args.warmup), stream, hbm)
         except Exception as e:  # reported, not fatal

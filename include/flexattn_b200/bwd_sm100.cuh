@@ -108,6 +108,9 @@ constexpr bool kDkSS = FA_BWD_DKSS != 0;
 #ifndef FA_BWD_REG_OTHER
 #define FA_BWD_REG_OTHER 64  // setmaxnreg of the producer / MMA warpgroup (160/64: +1..2 %, fewer spills)
 #endif
+#ifndef FA_BWD_PAIRED
+#define FA_BWD_PAIRED 0  // 1: phase A's exponents of plain / ALiBi scores as FFMA2 pairs
+#endif
 #ifndef FA_BWD_L2PF
 #define FA_BWD_L2PF 0  // 1: L2 prefetch of the next task's Q / dO tiles (one task ahead)
 #endif
@@ -673,12 +676,26 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float4 c4 = ct4[i4];
               const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
               float pv[4], gv[4];
+              float xp[4];  // plain / ALiBi: the exponents of the 4 scores as two FFMA2 pairs
+              if constexpr (FA_BWD_PAIRED != 0 && (ScoreT::kKind == 0 || ScoreT::kKind == 1)) {
+#pragma unroll
+                for (int e = 0; e < 4; e += 2) {
+                  float2 add = make_float2(cv[e], cv[e + 1]);
+                  if constexpr (ScoreT::kKind == 1) add = __fadd2_rn(add, make_float2(rowc, rowc));
+                  const float2 xx = __ffma2_rn(make_float2(__uint_as_float(sr[i4 * 4 + e]), __uint_as_float(sr[i4 * 4 + e + 1])),
+                                               make_float2(colc.c, colc.c), add);
+                  xp[e] = xx.x;
+                  xp[e + 1] = xx.y;
+                }
+              }
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const int ii = i4 * 4 + e;
                 const float sv = __uint_as_float(sr[ii]);
                 float x;
-                if constexpr (ScoreT::kKind == 0) {
+                if constexpr (FA_BWD_PAIRED != 0 && (ScoreT::kKind == 0 || ScoreT::kKind == 1)) {
+                  x = xp[e];
+                } else if constexpr (ScoreT::kKind == 0) {
                   x = fmaf(sv, colc.c, cv[e]);
                 } else if constexpr (ScoreT::kKind == 1) {
                   x = fmaf(sv, colc.c, cv[e] + rowc);

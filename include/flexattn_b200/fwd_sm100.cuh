@@ -58,6 +58,9 @@ namespace {  // internal linkage: every including translation unit has its own c
 #ifndef FA_FWD_ALIBI_TAB
 #define FA_FWD_ALIBI_TAB 0  // 1: ALiBi column term slope*log2e*i from a per-item smem table
 #endif
+#ifndef FA_FWD_ALIBI_REG
+#define FA_FWD_ALIBI_REG 1  // ALiBi column term of a 32-column chunk in registers (float2 pairs): +5 % C2
+#endif
 #ifndef FA_FWD_SPLITP
 #define FA_FWD_SPLITP 0  // 1: every score variant releases P in two halves
 #endif
@@ -436,6 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         sm.coltab[t][n & 1][row] = -__ldg(score.p.slopes + it.h) * kLog2e * static_cast<float>(row);
         named_bar_sync(1 + t, 128);
       }
+      // ALiBi in registers: the column term step·i of a 32-column chunk as 16 float2 pairs (per
+      // item: the slope is the head's); the chunk's offset (row term + step·32·chunk) joins the
+      // max and the exponent per chunk, so a pair of scores costs one FFMA2
+      constexpr bool kAlibiReg = FA_FWD_ALIBI_REG != 0 && ScoreT::kKind == 1;
+      float2 abias[16];
+      if constexpr (kAlibiReg) {
+        const float st = -__ldg(score.p.slopes + it.h) * kLog2e;
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) abias[k2] = make_float2(st * (2 * k2), st * (2 * k2 + 1));
+      }
       float m = -INFINITY, l = 0.f;
       bool any_blocks = false;
       for (int j = 0; j < len; ++j) {
@@ -471,7 +484,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 128; i += 2) {
             float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
-            if constexpr (kAlibiTab) {
+            if constexpr (kAlibiReg) {
+              // chunk-relative: s·c + step·(i mod 32); max accumulator = the chunk
+              const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), abias[(i & 31) >> 1]);
+              v0 = vv.x;
+              v1 = vv.y;
+            } else if constexpr (kAlibiTab) {
               // s·c + column term; the row term (rowc.base) joins the max and the exponent
               const float2 ct = *reinterpret_cast<const float2*>(ctab + i);
               const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), ct);
@@ -490,11 +508,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               r[i] = __float_as_uint(v0);
               r[i + 1] = __float_as_uint(v1);
             }
-            mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], v0, v1);
+            if constexpr (kAlibiReg) mx4[i >> 5] = fmax3(mx4[i >> 5], v0, v1);
+            else mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], v0, v1);
           }
         };
         if (full) pass1(std::false_type{});
         else pass1(std::true_type{});
+        float coff[4] = {0.f, 0.f, 0.f, 0.f};  // ALiBi chunk offsets (kAlibiReg)
+        if constexpr (kAlibiReg) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            coff[cc] = rowc.shifted(32 * cc).base;
+            mx4[cc] += coff[cc];  // -inf stays -inf
+          }
+        }
         float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
         if constexpr (kPlain) mx *= rowc.c;
         if constexpr (kAlibiTab) mx += rowc.base;  // -inf stays -inf
@@ -561,8 +588,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           auto exp_all = [&](auto emulate) {
 #pragma unroll
             for (int i = 0; i < 64; ++i) {
+              float2 nmc = nm2;
+              if constexpr (kAlibiReg) nmc = make_float2(nm2.x + coff[i >> 4], nm2.y + coff[i >> 4]);
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
-                                          xs2, nm2);
+                                          xs2, nmc);
               float2 pv;
               if (decltype(emulate)::value && (i % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
                 pv = exp2_poly2(x);

@@ -61,6 +61,12 @@ namespace {  // internal linkage: every including translation unit has its own c
 #ifndef FA_FWD_ALIBI_REG
 #define FA_FWD_ALIBI_REG 1  // ALiBi column term of a 32-column chunk in registers (float2 pairs): +5 % C2
 #endif
+#ifndef FA_FWD_FUSED
+#define FA_FWD_FUSED 0  // 1: stale-max single pass (max and exponentials together) after a row's first block (-7 % C2/C3, off)
+#endif
+#ifndef FA_FWD_WARP_ARRIVE
+#define FA_FWD_WARP_ARRIVE 0  // 1: P release by one arrival per warp (after __syncwarp) instead of per thread
+#endif
 #ifndef FA_FWD_SPLITP
 #define FA_FWD_SPLITP 0  // 1: every score variant releases P in two halves
 #endif
@@ -161,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_free[t], 1);
       mbar_init(&sm.s_full[t], 1);
       // split P (soft-capped scores): one arrival per warp and half; else per thread, [1] only
-      mbar_init(&sm.p_full[t][0], split_p<ScoreT>() ? 4 : 128);
-      mbar_init(&sm.p_full[t][1], split_p<ScoreT>() ? 4 : 128);
+      mbar_init(&sm.p_full[t][0], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
+      mbar_init(&sm.p_full[t][1], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
@@ -479,52 +485,130 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_ld();
         if (row == 0) ftrace(p, gs, 16);
+        // score_mod (log2 domain) and mask_mod of the score pair (i, i+1), from r
+        auto score_pair = [&](int i, auto masked, float& v0, float& v1) {
+          v0 = __uint_as_float(r[i]);
+          v1 = __uint_as_float(r[i + 1]);
+          if constexpr (kAlibiReg) {
+            // chunk-relative: s·c + step·(i mod 32); max accumulator = the chunk
+            const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), abias[(i & 31) >> 1]);
+            v0 = vv.x;
+            v1 = vv.y;
+          } else if constexpr (kAlibiTab) {
+            // s·c + column term; the row term (rowc.base) joins the max and the exponent
+            const float2 ct = *reinterpret_cast<const float2*>(ctab + i);
+            const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), ct);
+            v0 = vv.x;
+            v1 = vv.y;
+          } else if constexpr (!kPlain) {
+            const auto rc = rowc.shifted(i & ~31);
+            v0 = rc.log2(v0, i & 31);
+            v1 = rc.log2(v1, (i + 1) & 31);
+          }
+          if constexpr (decltype(masked)::value) {
+            v0 = ((bits[i >> 5] >> (i & 31)) & 1u) ? v0 : -INFINITY;
+            v1 = ((bits[i >> 5] >> ((i + 1) & 31)) & 1u) ? v1 : -INFINITY;
+          }
+        };
+        auto max_acc = [&](float (&acc)[4], int i, float v0, float v1) {
+          if constexpr (kAlibiReg) acc[i >> 5] = fmax3(acc[i >> 5], v0, v1);
+          else acc[(i >> 1) & 3] = fmax3(acc[(i >> 1) & 3], v0, v1);
+        };
+        // the row max of the block from the accumulators (ALiBi chunk offsets added, a plain
+        // score scaled once)
+        float coff[4] = {0.f, 0.f, 0.f, 0.f};  // ALiBi chunk offsets (kAlibiReg)
+        if constexpr (kAlibiReg) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) coff[cc] = rowc.shifted(32 * cc).base;
+        }
+        auto block_max = [&](float (&acc)[4]) {
+          if constexpr (kAlibiReg) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) acc[cc] += coff[cc];  // -inf stays -inf
+          }
+          float mx = fmaxf(fmaxf(acc[0], acc[1]), fmaxf(acc[2], acc[3]));
+          if constexpr (kPlain) mx *= rowc.c;
+          if constexpr (kAlibiTab) mx += rowc.base;  // -inf stays -inf
+          return mx;
+        };
+        constexpr bool kSplitP = split_p<ScoreT>();
+        const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
+        // Stale-max single pass (every block but a row's first): the exponentials use the
+        // running max m while the block max is still being accumulated, so the MUFU work starts
+        // right after the TMEM load instead of after a separate max pass. If the block raised a
+        // row's max past the lazy-rescale threshold (or the row had no max yet) the warp
+        // discards the pass and runs the two-pass path below; otherwise the result is exactly
+        // what the two-pass path computes (it keeps the stale max too).
+        constexpr bool kFused = FA_FWD_FUSED != 0 && !kSplitP && !kAlibiTab;
+        if constexpr (kFused) {
+          if (__any_sync(0xffffffffu, m != -INFINITY)) {
+            const float msub0 = (m == -INFINITY) ? 0.f : m;
+            float2 nmc[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) nmc[cc] = make_float2(coff[cc] - msub0, coff[cc] - msub0);
+            float fm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            float2 fl[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                            make_float2(0.f, 0.f)};
+            uint32_t pk[64];
+            auto fpass = [&](auto masked) {
+#pragma unroll
+              for (int i = 0; i < 128; i += 2) {
+                float v0, v1;
+                score_pair(i, masked, v0, v1);
+                max_acc(fm4, i, v0, v1);
+                const float2 x = __ffma2_rn(make_float2(v0, v1), xs2, nmc[i >> 5]);
+                const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+                fl[(i >> 1) & 3] = __fadd2_rn(fl[(i >> 1) & 3], pv);
+                pk[i >> 1] = pack_bf16(pv.x, pv.y);
+              }
+            };
+            if (full) fpass(std::false_type{});
+            else fpass(std::true_type{});
+            const float fmx = block_max(fm4);
+            const float fm_new = fmaxf(m, fmx);
+            const bool redo = (m == -INFINITY) ? (fm_new != -INFINITY) : (fm_new > m + kRescaleThreshold);
+            if (!__any_sync(0xffffffffu, redo)) {
+              tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+              tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+              tmem_wait_st();
+              tc_fence_before();
+              if constexpr (FA_FWD_WARP_ARRIVE != 0) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.p_full[t][1]);
+              } else {
+                mbar_arrive(&sm.p_full[t][1]);
+              }
+              const float2 l01 = __fadd2_rn(fl[0], fl[1]), l23 = __fadd2_rn(fl[2], fl[3]);
+              const float2 lt = __fadd2_rn(l01, l23);
+              l += lt.x + lt.y;
+              if (row == 0) ftrace(p, gs, t * 2 + 1);
+              ++gs;
+              continue;  // (not a flag: r must be dead on this path for the register allocator)
+            } else {
+              // the scores are still in TMEM (P has not been written): reload them
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc)
+                tmem_ld32(s_tm + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[cc * 32]));
+              tmem_wait_ld();
+            }
+          }
+        }
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         auto pass1 = [&](auto masked) {
 #pragma unroll
           for (int i = 0; i < 128; i += 2) {
-            float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
-            if constexpr (kAlibiReg) {
-              // chunk-relative: s·c + step·(i mod 32); max accumulator = the chunk
-              const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), abias[(i & 31) >> 1]);
-              v0 = vv.x;
-              v1 = vv.y;
-            } else if constexpr (kAlibiTab) {
-              // s·c + column term; the row term (rowc.base) joins the max and the exponent
-              const float2 ct = *reinterpret_cast<const float2*>(ctab + i);
-              const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), ct);
-              v0 = vv.x;
-              v1 = vv.y;
-            } else if constexpr (!kPlain) {
-              const auto rc = rowc.shifted(i & ~31);
-              v0 = rc.log2(v0, i & 31);
-              v1 = rc.log2(v1, (i + 1) & 31);
-            }
-            if constexpr (decltype(masked)::value) {
-              v0 = ((bits[i >> 5] >> (i & 31)) & 1u) ? v0 : -INFINITY;
-              v1 = ((bits[i >> 5] >> ((i + 1) & 31)) & 1u) ? v1 : -INFINITY;
-            }
+            float v0, v1;
+            score_pair(i, masked, v0, v1);
             if constexpr (!kPlain || decltype(masked)::value) {
               r[i] = __float_as_uint(v0);
               r[i + 1] = __float_as_uint(v1);
             }
-            if constexpr (kAlibiReg) mx4[i >> 5] = fmax3(mx4[i >> 5], v0, v1);
-            else mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], v0, v1);
+            max_acc(mx4, i, v0, v1);
           }
         };
         if (full) pass1(std::false_type{});
         else pass1(std::true_type{});
-        float coff[4] = {0.f, 0.f, 0.f, 0.f};  // ALiBi chunk offsets (kAlibiReg)
-        if constexpr (kAlibiReg) {
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            coff[cc] = rowc.shifted(32 * cc).base;
-            mx4[cc] += coff[cc];  // -inf stays -inf
-          }
-        }
-        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-        if constexpr (kPlain) mx *= rowc.c;
-        if constexpr (kAlibiTab) mx += rowc.base;  // -inf stays -inf
+        const float mx = block_max(mx4);
         // lazy rescale (warp-uniform decision; tcgen05.ld/st are warp-collective)
         const float m_new = fmaxf(m, mx);
         const bool need = (m != -INFINITY) && (m_new > m + kRescaleThreshold);
@@ -548,8 +632,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // With a soft-capped score (tanh + exp2 per score: the MUFU is the bottleneck) each half
         // releases its PV MMAs on its own (p_full[t][half]) and, in full blocks, a quarter of
         // the exponentials run on the FMA pipe (exp2_poly2); measured slower for the others.
-        constexpr bool kSplitP = split_p<ScoreT>();
-        const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
         float nmv = -msub;
         if constexpr (kAlibiTab) nmv = rowc.base - msub;  // the ALiBi row term rejoins here
         const float2 nm2 = make_float2(nmv, nmv);
@@ -606,12 +688,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&sm.p_full[t][1]);
+          if constexpr (FA_FWD_WARP_ARRIVE != 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full[t][1]);
+          } else {
+            mbar_arrive(&sm.p_full[t][1]);
+          }
         }
-        if (row == 0) ftrace(p, gs, 18);
         const float2 l01 = __fadd2_rn(ls[0], ls[1]), l23 = __fadd2_rn(ls[2], ls[3]);
         const float2 lt = __fadd2_rn(l01, l23);
         l += lt.x + lt.y;
+        if (row == 0) ftrace(p, gs, 18);
         if (row == 0) ftrace(p, gs, t * 2 + 1);
         ++gs;
       }

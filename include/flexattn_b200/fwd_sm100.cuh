@@ -68,8 +68,12 @@ namespace {  // internal linkage: every including translation unit has its own c
 #define FA_FWD_WARP_ARRIVE 0  // 1: P release by one arrival per warp (after __syncwarp) instead of per thread
 #endif
 #ifndef FA_FWD_SPLITP
-#define FA_FWD_SPLITP 0  // 1: every score variant releases P in two halves
+#define FA_FWD_SPLITP 1  // every score variant releases P in parts (C2 +1.4 %, C3 +2.2 %)
 #endif
+#ifndef FA_FWD_PPARTS
+#define FA_FWD_PPARTS 2  // parts of P released separately (2 or 4)
+#endif
+constexpr int kPParts = FA_FWD_PPARTS;
 template <class ScoreT>
 constexpr bool split_p() { return FA_FWD_SPLITP != 0 || !ScoreT::kUnitGrad; }
 constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, 2 idle) warpgroup
@@ -128,7 +132,7 @@ struct alignas(1024) Smem {
   uint64_t q_full[2], q_free[2];
   uint64_t k_full[Cfg<D>::kStages], v_full[Cfg<D>::kStages];
   uint64_t k_empty[Cfg<D>::kStages], v_empty[Cfg<D>::kStages];  // released separately
-  uint64_t s_full[2], p_full[2][2], o_full[2];  // p_full[tile][half of the kv block]
+  uint64_t s_full[2], p_full[2][kPParts], o_full[2];  // p_full[tile][part of the kv block]
   uint64_t item_full[2], item_empty[2];
   uint32_t tmem_base;
 };
@@ -167,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.q_free[t], 1);
       mbar_init(&sm.s_full[t], 1);
       // split P (soft-capped scores): one arrival per warp and half; else per thread, [1] only
-      mbar_init(&sm.p_full[t][0], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
-      mbar_init(&sm.p_full[t][1], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
+      for (int pp = 0; pp < kPParts; ++pp)
+        mbar_init(&sm.p_full[t][pp], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
@@ -314,19 +318,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
-      // O_t += P_t V: the first 64 kv (P columns 0-31) as soon as the softmax released them,
-      // the rest when the second half of P is in TMEM
+      // O_t += P_t V: each part of the kv block (128 / kPParts kv, P columns of that part) as
+      // soon as the softmax released it
       constexpr bool kSplitP = split_p<ScoreT>();  // see the softmax
       auto issue_pv = [&](int t, int st, bool acc, uint32_t ph) {
         const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.v[st]), C::kChunkBytes, 1024);
         if constexpr (kSplitP) {
+          constexpr int kSteps = (kTile / 16) / kPParts;
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
+          for (int hf = 0; hf < kPParts; ++hf) {
             mbar_wait(&sm.p_full[t][hf], ph);
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll
-              for (int kk = hf * 4; kk < hf * 4 + 4; ++kk)
+              for (int kk = hf * kSteps; kk < hf * kSteps + kSteps; ++kk)
                 umma_ts(tm + 256 + t * D, tm + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
                         (acc || kk > 0) ? 1u : 0u);
             }
@@ -629,22 +634,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (row == 0) ftrace(p, gs, 17);
         const float msub = (m == -INFINITY) ? 0.f : m;
         // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1).
-        // With a soft-capped score (tanh + exp2 per score: the MUFU is the bottleneck) each half
-        // releases its PV MMAs on its own (p_full[t][half]) and, in full blocks, a quarter of
-        // the exponentials run on the FMA pipe (exp2_poly2); measured slower for the others.
+        // Each part of P releases its PV MMAs on its own (p_full[t][part]) so the tensor core
+        // starts on the first kv of the block while the exponentials of the rest run; in full
+        // blocks one exponential pair in FA_FWD_EMU_EVERY runs on the FMA pipe (exp2_poly2).
         float nmv = -msub;
         if constexpr (kAlibiTab) nmv = rowc.base - msub;  // the ALiBi row term rejoins here
         const float2 nm2 = make_float2(nmv, nmv);
         float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
         if constexpr (kSplitP) {
-          auto exp_half = [&](int hf, auto emulate) {
-            uint32_t pk[32];
+          constexpr int kPairs = 64 / kPParts;  // packed P columns per part
+          auto exp_part = [&](int hf, auto emulate) {
+            uint32_t pk[kPairs];
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const int i = hf * 32 + k;
+            for (int k = 0; k < kPairs; ++k) {
+              const int i = hf * kPairs + k;
+              float2 nmc = nm2;
+              if constexpr (kAlibiReg) nmc = make_float2(nm2.x + coff[i >> 4], nm2.y + coff[i >> 4]);
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
-                                          xs2, nm2);
+                                          xs2, nmc);
               float2 pv;
               if (decltype(emulate)::value && FA_FWD_EMU != 0 && (k % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
                 pv = exp2_poly2(x);
@@ -652,18 +660,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               ls[k & 3] = __fadd2_rn(ls[k & 3], pv);
               pk[k] = pack_bf16(pv.x, pv.y);
             }
-            tmem_st32(s_tm + hf * 32, pk);
+            if constexpr (kPairs == 32) tmem_st32(s_tm + hf * kPairs, *reinterpret_cast<uint32_t(*)[32]>(pk));
+            else tmem_st16(s_tm + hf * kPairs, *reinterpret_cast<uint32_t(*)[16]>(pk));
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full[t][hf]);
           };
           if (full) {
-            exp_half(0, std::true_type{});
-            exp_half(1, std::true_type{});
+#pragma unroll
+            for (int hf = 0; hf < kPParts; ++hf) exp_part(hf, std::true_type{});
           } else {
-            exp_half(0, std::false_type{});
-            exp_half(1, std::false_type{});
+#pragma unroll
+            for (int hf = 0; hf < kPParts; ++hf) exp_part(hf, std::false_type{});
           }
         } else {
           uint32_t pk[64];

@@ -67,6 +67,9 @@ namespace {  // internal linkage: every including translation unit has its own c
 #ifndef FA_FWD_WARP_ARRIVE
 #define FA_FWD_WARP_ARRIVE 0  // 1: P release by one arrival per warp (after __syncwarp) instead of per thread
 #endif
+#ifndef FA_FWD_OSTAGE
+#define FA_FWD_OSTAGE 1  // epilogue O stores coalesced through a per-warp smem tile
+#endif
 #ifndef FA_FWD_SPLITP
 #define FA_FWD_SPLITP 1  // every score variant releases P in parts (C2 +1.4 %, C3 +2.2 %)
 #endif
@@ -101,7 +104,7 @@ struct FwdParams {
 #ifndef FA_FWD_TRACE_BUILD
 #define FA_FWD_TRACE_BUILD 0
 #endif
-constexpr int kFTraceSteps = 512, kFTraceEv = 24;
+constexpr int kFTraceSteps = 512, kFTraceEv = 32;
 __device__ __forceinline__ void ftrace(const FwdParams& p, int step, int ev) {
   if constexpr (FA_FWD_TRACE_BUILD != 0) {
     if (p.trace != nullptr && blockIdx.x == 0 && step < kFTraceSteps && (threadIdx.x & 31) == 0) {
@@ -127,6 +130,7 @@ struct alignas(1024) Smem {
   uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   int32_t ulist[2][kMaxCols];
   float coltab[2][2][kTile];  // [tile][item parity][kv]: ALiBi column term (FA_FWD_ALIBI_TAB)
+  uint8_t ostage[8][32 * 64];  // epilogue: per softmax warp, 32 rows x 32 bf16 (swizzled)
   int32_t ulen[2];
   int32_t uitem[2];   // work item of the buffer, -1 = no more work
   uint64_t q_full[2], q_free[2];
@@ -258,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sm.ulen[buf] = len;
         mbar_arrive(&sm.item_full[buf]);
+        ftrace(p, n, 19);
         // ---- Q tiles ----
         for (int t = 0; t < 2; ++t) {
           mbar_wait(&sm.q_free[t], (n & 1) ^ 1);
@@ -266,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_3d(sm.q[t] + ch * C::kChunkBytes, &tmQ, &sm.q_full[t], ch * 64,
                         (r0 + t) * kTile, it.b * p.Hq + it.h);
         }
+        ftrace(p, n, 20);
         // ---- K/V blocks ----
         const int kb = p.Bkv == 1 ? 0 : it.b, kh = it.h / p.G;
         for (int j = 0; j < len; ++j, ++kv_it) {
@@ -274,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int colb = static_cast<int>(static_cast<uint32_t>(sm.ulist[buf][j]) & kColMask);
           mbar_wait(&sm.k_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
           ftrace(p, kv_it, 12);
+          if (j == 0) ftrace(p, n, 26);
           mbar_expect_tx(&sm.k_full[st], C::kTileBytes);
           for (int ch = 0; ch < C::kChunks; ++ch)
             tma_load_3d(sm.k[st] + ch * C::kChunkBytes, &tmK, &sm.k_full[st], ch * 64,
@@ -357,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* U = reinterpret_cast<const uint32_t*>(sm.ulist[buf]);
         mbar_wait(&sm.q_full[0], n & 1);
         mbar_wait(&sm.q_full[1], n & 1);
+        ftrace(p, n, 21);
         tc_fence_after();
         // last step that reads Q_t: Q_t's smem is released (q_free) as soon as that QK completes
         int last_qk[2] = {-1, -1};
@@ -373,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&sm.k_full[st0], (kv_it / C::kStages) & 1);
           tc_fence_after();
           const uint32_t e0 = U[0];
+          ftrace(p, n, 24);
           if (e0 & kIn0) { issue_qk(0, st0); if (last_qk[0] == 0) commit(&sm.q_free[0]); }
           if (e0 & kIn1) { issue_qk(1, st0); if (last_qk[1] == 0) commit(&sm.q_free[1]); }
           commit(&sm.k_empty[st0]);
@@ -416,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         kv_it += len;
         for (int t = 0; t < 2; ++t) commit(&sm.o_full[t]);
+        ftrace(p, n, 22);
         if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
       }
     }
@@ -713,11 +723,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ---- epilogue: O / l -> bf16, lse ----
       mbar_wait(&sm.o_full[t], n & 1);
+      if (row == 0 && t == 0) ftrace(p, n, 23);
       tc_fence_after();
       const bool valid = qi < p.Lq;
       const long long slot = (static_cast<long long>(it.b) * p.Hq + it.h) * p.Lq + qi;
       __nv_bfloat16* orow = p.out + slot * D;
-      if (any_blocks) {
+      if (FA_FWD_OSTAGE != 0 && any_blocks) {
+        // 32 columns at a time through a per-warp smem tile, stored as 8 rows x 64 contiguous
+        // bytes per instruction (a row-per-thread store touches 32 lines per instruction and
+        // kept the LSU busy for ~5000 cycles at every item boundary)
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        uint8_t* stg = sm.ostage[warp];
+        const int qrow0 = (2 * it.pair + t) * kTile + wq * 32;
+        const long long slot0 = (static_cast<long long>(it.b) * p.Hq + it.h) * p.Lq;
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t r0[32];
+          tmem_ld32(o_tm + cc * 32, r0);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(r0[8 * k + 0]) * inv, __uint_as_float(r0[8 * k + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(r0[8 * k + 2]) * inv, __uint_as_float(r0[8 * k + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(r0[8 * k + 4]) * inv, __uint_as_float(r0[8 * k + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(r0[8 * k + 6]) * inv, __uint_as_float(r0[8 * k + 7]) * inv);
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = w;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i8 = 0; i8 < 4; ++i8) {
+            const int rr = i8 * 8 + (lane >> 2), sg = lane & 3;
+            const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 64 + ((sg ^ ((rr >> 1) & 3)) << 4));
+            if (qrow0 + rr < p.Lq)
+              *reinterpret_cast<uint4*>(p.out + (slot0 + qrow0 + rr) * D + cc * 32 + sg * 8) = w;
+          }
+          __syncwarp();
+        }
+      } else if (any_blocks) {
         const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
         for (int cc = 0; cc < D / 64; ++cc) {
@@ -745,6 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int v4 = 0; v4 < D / 8; ++v4) dst[v4] = make_uint4(0, 0, 0, 0);
       }
       if (valid) p.lse[slot] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+      if (row == 0 && t == 0) ftrace(p, n, 25);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
@@ -813,6 +857,11 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
       const long long* e = h + s * kFTraceEv;
       fprintf(stderr, "[fwd trace] block %d: K issued %lld  V issued %lld  MMA wants V %lld  V seen %lld\n", s,
               e[12] - t0, e[13] - t0, e[15] - t0, e[14] - t0);
+    }
+    for (int n = 0; n < 12; ++n) {
+      const long long* e = h + n * kFTraceEv;
+      fprintf(stderr, "[fwd trace] item %d: list %lld  Q issued %lld  K0 issued %lld  MMA has Q %lld  first QK %lld  MMA item end %lld  epi0 %lld..%lld\n", n,
+              e[19] - t0, e[20] - t0, e[26] - t0, e[21] - t0, e[24] - t0, e[22] - t0, e[23] - t0, e[25] - t0);
     }
     double sm0 = 0, per = 0;
     int cnt = 0;

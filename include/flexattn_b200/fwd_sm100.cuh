@@ -68,7 +68,10 @@ namespace {  // internal linkage: every including translation unit has its own c
 #define FA_FWD_WARP_ARRIVE 0  // 1: P release by one arrival per warp (after __syncwarp) instead of per thread
 #endif
 #ifndef FA_FWD_OSTAGE
-#define FA_FWD_OSTAGE 1  // epilogue O stores coalesced through a per-warp smem tile
+#define FA_FWD_OSTAGE 2  // epilogue O through a per-warp smem tile: 1 coalesced st.global, 2 TMA store
+#endif
+#ifndef FA_FWD_EARLY_O
+#define FA_FWD_EARLY_O 1  // O_t released to the epilogue right after tile t's last PV
 #endif
 #ifndef FA_FWD_SPLITP
 #define FA_FWD_SPLITP 1  // every score variant releases P in parts (C2 +1.4 %, C3 +2.2 %)
@@ -130,7 +133,7 @@ struct alignas(1024) Smem {
   uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   int32_t ulist[2][kMaxCols];
   float coltab[2][2][kTile];  // [tile][item parity][kv]: ALiBi column term (FA_FWD_ALIBI_TAB)
-  uint8_t ostage[8][32 * 64];  // epilogue: per softmax warp, 32 rows x 32 bf16 (swizzled)
+  alignas(512) uint8_t ostage[8][32 * 64];  // epilogue: per softmax warp, 32 rows x 32 bf16 (64-byte swizzle)
   int32_t ulen[2];
   int32_t uitem[2];   // work item of the buffer, -1 = no more work
   uint64_t q_full[2], q_free[2];
@@ -160,7 +163,8 @@ template <int D, class MaskT, class ScoreT>
 __global__ void __launch_bounds__(kThreads, 1)
     flex_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
-                          const __grid_constant__ CUtensorMap tmV, const FwdParams p, MaskT mask,
+                          const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmO, const FwdParams p, MaskT mask,
                           ScoreT score) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -407,6 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               p_phase[t] ^= 1;
               first_pv[t] = false;
               ++mg[t];
+              // O_t is final once tile t's last PV completes: its epilogue need not wait for
+              // the other tile's last PV
+              if (FA_FWD_EARLY_O != 0 && last_qk[t] == j) commit(&sm.o_full[t]);
             }
             if (en & in_bit) {
               if (!k1_ready) {
@@ -424,7 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           commit(&sm.v_empty[st]);
         }
         kv_it += len;
-        for (int t = 0; t < 2; ++t) commit(&sm.o_full[t]);
+        for (int t = 0; t < 2; ++t)
+          if (FA_FWD_EARLY_O == 0 || last_qk[t] < 0) commit(&sm.o_full[t]);
         ftrace(p, n, 22);
         if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
       }
@@ -741,6 +749,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t r0[32];
           tmem_ld32(o_tm + cc * 32, r0);
           tmem_wait_ld();
+          if (row == 0 && t == 0) ftrace(p, n, 27 + cc);
+          if constexpr (FA_FWD_OSTAGE == 2) {  // the previous TMA store has read the tile
+            if (lane == 0) bulk_wait_group_read<0>();
+            __syncwarp();
+          }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint4 w;
@@ -749,6 +762,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             w.z = pack_bf16(__uint_as_float(r0[8 * k + 4]) * inv, __uint_as_float(r0[8 * k + 5]) * inv);
             w.w = pack_bf16(__uint_as_float(r0[8 * k + 6]) * inv, __uint_as_float(r0[8 * k + 7]) * inv);
             *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = w;
+          }
+          if constexpr (FA_FWD_OSTAGE == 2) {
+            // the tile is in the SWIZZLE_64B layout: one TMA store of 32 rows x 32 columns
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&tmO, stg, cc * 32, qrow0, it.b * p.Hq + it.h);
+              bulk_commit_group();
+            }
+            continue;
           }
           __syncwarp();
 #pragma unroll
@@ -793,6 +816,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
     }
+    if constexpr (FA_FWD_OSTAGE == 2) {
+      if (lane == 0) bulk_wait_group<0>();  // the epilogue's TMA stores have landed
+      __syncwarp();
+    }
     FA_FWD_TEARDOWN();
   }
 #undef FA_FWD_TEARDOWN
@@ -802,9 +829,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, class MaskT, class ScoreT>
 fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
               const BmView& bm, MaskT mask, ScoreT score, cudaStream_t st) {
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo{};
   fa_status s;
   if ((s = make_map(&mq, q, g.B * g.Hq, g.Lq, D)) != FA_OK) return s;
+  if (FA_FWD_OSTAGE == 2) {
+    const CUresult r = encode_o32_map(&mo, o, g.B * g.Hq, g.Lq, D);
+    FA_REQUIRE(r == CUDA_SUCCESS, FA_CUDA_ERROR,
+               "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  }
   if ((s = make_map(&mk, k, g.Bkv * g.Hkv, g.Lkv, D)) != FA_OK) return s;
   if ((s = make_map(&mv, v, g.Bkv * g.Hkv, g.Lkv, D)) != FA_OK) return s;
   FwdParams p{};
@@ -831,7 +863,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();
   if (grid <= 0) return FA_OK;
-  kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, p, mask, score);
+  kern<<<grid, kThreads, smem, st>>>(mq, mk, mv, mo, p, mask, score);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
   if (trace != nullptr) {  // debug: per-step events of CTA 0 (tile 0 and 1)
@@ -860,8 +892,9 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
     }
     for (int n = 0; n < 12; ++n) {
       const long long* e = h + n * kFTraceEv;
-      fprintf(stderr, "[fwd trace] item %d: list %lld  Q issued %lld  K0 issued %lld  MMA has Q %lld  first QK %lld  MMA item end %lld  epi0 %lld..%lld\n", n,
-              e[19] - t0, e[20] - t0, e[26] - t0, e[21] - t0, e[24] - t0, e[22] - t0, e[23] - t0, e[25] - t0);
+      fprintf(stderr, "[fwd trace] item %d: list %lld  Q issued %lld  K0 issued %lld  MMA has Q %lld  first QK %lld  MMA item end %lld  epi0 %lld..%lld (ld %lld %lld %lld %lld)\n", n,
+              e[19] - t0, e[20] - t0, e[26] - t0, e[21] - t0, e[24] - t0, e[22] - t0, e[23] - t0, e[25] - t0,
+              e[27] - e[23], e[28] - e[23], e[29] - e[23], e[30] - e[23]);
     }
     double sm0 = 0, per = 0;
     int cnt = 0;

@@ -161,6 +161,19 @@ inline CUresult encode_store_map(CUtensorMap* map, const void* base, int bh, int
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
+// 3-D map over a (BH, L, D) bf16 tensor with a (32, 32, 1) box and 64-byte swizzle: the forward's
+// epilogue stores O through it, 32 rows x 32 columns per warp (rows past L are clipped).
+inline CUresult encode_o32_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
+  EncodeTiledFn enc = get_encode();
+  if (enc == nullptr) return CUDA_ERROR_NOT_SUPPORTED;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(len), static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, static_cast<cuuint64_t>(len) * d * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
 inline CUresult encode_tile_map(CUtensorMap* map, const void* base, int bh, int len, int d) {
   return encode_store_map(map, base, bh, len, d, 128);
 }

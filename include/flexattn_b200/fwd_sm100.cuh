@@ -73,6 +73,9 @@ namespace {  // internal linkage: every including translation unit has its own c
 #ifndef FA_FWD_EARLY_O
 #define FA_FWD_EARLY_O 1  // O_t released to the epilogue right after tile t's last PV
 #endif
+#ifndef FA_FWD_LISTWARP
+#define FA_FWD_LISTWARP 1  // warp 10 builds the item lists (warp-parallel) while warp 8 loads Q
+#endif
 #ifndef FA_FWD_SPLITP
 #define FA_FWD_SPLITP 1  // every score variant releases P in parts (C2 +1.4 %, C3 +2.2 %)
 #endif
@@ -132,6 +135,9 @@ struct alignas(1024) Smem {
   uint8_t k[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   int32_t ulist[2][kMaxCols];
+  uint32_t ubits[4][kMaxCols / 32];  // FA_FWD_LISTWARP: the list builder's column bitmaps
+  int32_t claim_item[2];             // FA_FWD_LISTWARP: item handed to the list builder
+  uint64_t claim_full[2];
   float coltab[2][2][kTile];  // [tile][item parity][kv]: ALiBi column term (FA_FWD_ALIBI_TAB)
   alignas(512) uint8_t ostage[8][32 * 64];  // epilogue: per softmax warp, 32 rows x 32 bf16 (64-byte swizzle)
   int32_t ulen[2];
@@ -184,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
+      mbar_init(&sm.claim_full[t], 1);
     }
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&sm.k_full[s], 1);
@@ -221,7 +228,125 @@ __global__ void __launch_bounds__(kThreads, 1)
   } while (0)
   if (warp >= 8) {
     reg_dealloc<56>();
-    if (warp == 8 && lane == 0) {
+    if (FA_FWD_LISTWARP != 0 && warp == 8 && lane == 0) {
+      // ===================== TMA producer (lists built by warp 10) =====================
+      // claims an item, hands it to the list builder, loads its Q tiles while the list is
+      // being built, then streams the K/V blocks of the list
+      int kv_it = 0;
+      int item = static_cast<int>(blockIdx.x);
+      for (int n = 0;; ++n) {
+        const int buf = n & 1;
+        mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
+        sm.claim_item[buf] = item;
+        mbar_arrive(&sm.claim_full[buf]);
+        if (item >= p.num_items) break;
+        const Item it = decode_item(p, item);
+        const int r0 = 2 * it.pair;
+        // ---- Q tiles ----
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&sm.q_free[t], (n & 1) ^ 1);
+          mbar_expect_tx(&sm.q_full[t], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.q[t] + ch * C::kChunkBytes, &tmQ, &sm.q_full[t], ch * 64,
+                        (r0 + t) * kTile, it.b * p.Hq + it.h);
+        }
+        ftrace(p, n, 20);
+        mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
+        const int len = sm.ulen[buf];
+        // ---- K/V blocks ----
+        const int kb = p.Bkv == 1 ? 0 : it.b, kh = it.h / p.G;
+        for (int j = 0; j < len; ++j, ++kv_it) {
+          const int st = kv_it % C::kStages;
+          const int colb = static_cast<int>(static_cast<uint32_t>(sm.ulist[buf][j]) & kColMask);
+          mbar_wait(&sm.k_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          ftrace(p, kv_it, 12);
+          if (j == 0) ftrace(p, n, 26);
+          mbar_expect_tx(&sm.k_full[st], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.k[st] + ch * C::kChunkBytes, &tmK, &sm.k_full[st], ch * 64,
+                        colb * kTile, kb * p.Hkv + kh);
+          mbar_wait(&sm.v_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
+          ftrace(p, kv_it, 13);
+          mbar_expect_tx(&sm.v_full[st], C::kTileBytes);
+          for (int ch = 0; ch < C::kChunks; ++ch)
+            tma_load_3d(sm.v[st] + ch * C::kChunkBytes, &tmV, &sm.v_full[st], ch * 64,
+                        colb * kTile, kb * p.Hkv + kh);
+        }
+        item = static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
+      }
+    } else if (FA_FWD_LISTWARP != 0 && warp == 10) {
+      // ===================== list builder =====================
+      // the union of the item's two rows' visit lists in descending block order (blocks nearest
+      // the diagonal first, so the running max is established early): one bitmap word of 32
+      // block columns per lane, two global round trips
+      for (int n = 0;; ++n) {
+        const int buf = n & 1;
+        mbar_wait(&sm.claim_full[buf], (n >> 1) & 1);
+        const int item = *reinterpret_cast<volatile int32_t*>(&sm.claim_item[buf]);
+        if (item >= p.num_items) {
+          if (lane == 0) {
+            sm.uitem[buf] = -1;
+            mbar_arrive(&sm.item_full[buf]);
+          }
+          break;
+        }
+        const Item it = decode_item(p, item);
+        const int mb = p.bm_b == 1 ? 0 : it.b, mh = p.bm_h == 1 ? 0 : it.h;
+        const int r0 = 2 * it.pair, r1 = r0 + 1;
+        const long long s0 = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r0;
+        const int np0 = __ldg(p.kv_num + s0), nf0 = __ldg(p.full_num + s0);
+        const int np1 = r1 < p.rows ? __ldg(p.kv_num + s0 + 1) : 0;
+        const int nf1 = r1 < p.rows ? __ldg(p.full_num + s0 + 1) : 0;
+        const int32_t* pi0 = p.kv_idx + s0 * p.cols;
+        const int32_t* fi0 = p.full_idx + s0 * p.cols;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) sm.ubits[q4][lane] = 0u;
+        __syncwarp();
+        auto scatter = [&](const int32_t* idx, int cnt, int which) {
+          for (int i = lane; i < cnt; i += 32) {
+            const int c = __ldg(idx + i);
+            atomicOr(&sm.ubits[which][c >> 5], 1u << (c & 31));
+          }
+        };
+        scatter(pi0, np0, 0);
+        scatter(fi0, nf0, 1);
+        scatter(pi0 + p.cols, np1, 2);
+        scatter(fi0 + p.cols, nf1, 3);
+        __syncwarp();
+        const uint32_t bp0 = sm.ubits[0][lane], bf0 = sm.ubits[1][lane];
+        const uint32_t bp1 = sm.ubits[2][lane], bf1 = sm.ubits[3][lane];
+        const uint32_t in0 = bp0 | bf0, in1 = bp1 | bf1, any = in0 | in1;
+        const int cnt = __popc(any);
+        int incl = cnt;  // entries of this lane and the higher (larger column) lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_down_sync(0xffffffffu, incl, o);
+          if (lane + o < 32) incl += v;
+        }
+        int pos = incl - cnt;
+        for (uint32_t rem = any; rem != 0u;) {
+          const int bit = 31 - __clz(rem);
+          const uint32_t mbit = 1u << bit;
+          rem &= ~mbit;
+          uint32_t e = static_cast<uint32_t>(lane * 32 + bit);
+          if (in0 & mbit) e |= kIn0;
+          if (bf0 & mbit) e |= kFull0;
+          if (in1 & mbit) e |= kIn1;
+          if (bf1 & mbit) e |= kFull1;
+          sm.ulist[buf][pos++] = static_cast<int32_t>(e);
+        }
+        if (lane == 0) {
+          sm.ulen[buf] = incl;  // lane 0: all entries
+          sm.uitem[buf] = item;
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sm.item_full[buf]);
+          ftrace(p, n, 19);
+        }
+      }
+    } else if (FA_FWD_LISTWARP == 0 && warp == 8 && lane == 0) {
       // ===================== TMA producer =====================
       int kv_it = 0;
       for (int n = 0;; ++n) {

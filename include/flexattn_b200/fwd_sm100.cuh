@@ -778,8 +778,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float msub = (m == -INFINITY) ? 0.f : m;
         // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1).
         // Each part of P releases its PV MMAs on its own (p_full[t][part]) so the tensor core
-        // starts on the first kv of the block while the exponentials of the rest run; in full
-        // blocks one exponential pair in FA_FWD_EMU_EVERY runs on the FMA pipe (exp2_poly2).
+        // starts on the first kv of the block while the exponentials of the rest run. One
+        // exponential pair in FA_FWD_EMU_EVERY runs on the FMA pipe (exp2_poly2, exactly 0 for a
+        // masked score), chosen by column alone, so a block gives the same P whether it is
+        // classified full or partial (demote_full_to_partial / promote stay bit-exact).
         float nmv = -msub;
         if constexpr (kAlibiTab) nmv = rowc.base - msub;  // the ALiBi row term rejoins here
         const float2 nm2 = make_float2(nmv, nmv);
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         make_float2(0.f, 0.f)};
         if constexpr (kSplitP) {
           constexpr int kPairs = 64 / kPParts;  // packed P columns per part
-          auto exp_part = [&](int hf, auto emulate) {
+          auto exp_part = [&](int hf) {
             uint32_t pk[kPairs];
 #pragma unroll
             for (int k = 0; k < kPairs; ++k) {
@@ -797,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
                                           xs2, nmc);
               float2 pv;
-              if (decltype(emulate)::value && FA_FWD_EMU != 0 && (k % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
+              if (FA_FWD_EMU != 0 && (k % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
                 pv = exp2_poly2(x);
               else pv = make_float2(ex2(x.x), ex2(x.y));
               ls[k & 3] = __fadd2_rn(ls[k & 3], pv);
@@ -810,13 +812,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.p_full[t][hf]);
           };
-          if (full) {
 #pragma unroll
-            for (int hf = 0; hf < kPParts; ++hf) exp_part(hf, std::true_type{});
-          } else {
-#pragma unroll
-            for (int hf = 0; hf < kPParts; ++hf) exp_part(hf, std::false_type{});
-          }
+          for (int hf = 0; hf < kPParts; ++hf) exp_part(hf);
         } else {
           uint32_t pk[64];
           auto exp_all = [&](auto emulate) {

@@ -344,11 +344,12 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x for a pair of x <= 0 on the FMA/ALU pipes (no MUFU): x = r + f with r = round(x)
 // (magic-number rounding), f in [-0.5, 0.5]; 2^f by a degree-3 minimax polynomial (relative
 // error < 8e-5, far below bf16's 2^-9) and 2^r added into the exponent field. x is clamped at
-// -126 so large negative arguments give ~1e-38 instead of a wrapped exponent (2^f(0) < 1).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+// -126 so the exponent field cannot wrap; arguments below -126 (and -inf) return exactly 0.
+__device__ __forceinline__ float2 exp2_poly2(float2 x0) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
+  float2 x;
+  x.x = fmaxf(x0.x, -126.f);
+  x.y = fmaxf(x0.y, -126.f);
   const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
   const float2 rr = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
   const float2 f = __fadd2_rn(x, make_float2(-rr.x, -rr.y));
@@ -356,8 +357,9 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                          make_float2(0.24261115842f, 0.24261115842f));
   pl = __ffma2_rn(pl, f, make_float2(0.69326098995f, 0.69326098995f));
   pl = __ffma2_rn(pl, f, make_float2(0.99992807144f, 0.99992807144f));
-  return make_float2(__int_as_float(__float_as_int(pl.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(pl.y) + (__float_as_int(t.y) << 23)));
+  // below 2^-126 (and for a masked score, -inf) the result is 0, as ex2.approx.ftz gives
+  return make_float2(x0.x < -126.f ? 0.f : __int_as_float(__float_as_int(pl.x) + (__float_as_int(t.x) << 23)),
+                     x0.y < -126.f ? 0.f : __int_as_float(__float_as_int(pl.y) + (__float_as_int(t.y) << 23)));
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float y;

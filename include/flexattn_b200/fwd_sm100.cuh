@@ -7,19 +7,25 @@
 // query tiles (block rows 2p, 2p+1) of one (b, h):
 //   warps 0-3  softmax/correction/epilogue for tile 0   (thread = query row)
 //   warps 4-7  the same for tile 1
-//   warps 10-11 idle (they complete the third warpgroup for setmaxnreg)
-//   warp  8    TMA producer: merges both rows' kv lists (partial + full) into a
-//              union list in smem (descending block order; any order is exact
-//              math, descending keeps the running max stable),
-//              then streams Q (once) and K_j, V_j (per visited block) with
+//   warp  8    TMA producer: claims items (dynamic scheduler), loads the item's Q
+//              tiles, then streams K_j, V_j (per visited block) with
 //              cp.async.bulk.tensor into a 2-stage (D=128) ring. Empty blocks
 //              are never loaded.
+//   warp  10   list builder: the union of the two rows' visit lists (partial +
+//              full) in descending block order (any order is exact math;
+//              descending keeps the running max stable), built from per-lane
+//              column bitmaps while warp 8 loads Q
+//   warp  11   idle (completes the third warpgroup for setmaxnreg)
 //   warp  9    MMA issuer (warp-uniform control, one elected lane issues): S_t = Q_t K_j^T (SS, TMEM fp32) and
 //              O_t += P_t V_j (TS: P from TMEM as bf16, V from smem, MN-major),
 //              ordered  QK0 QK1 | PV0(j) QK0(j+1) PV1(j) QK1(j+1) | ...  so the
-//              two tiles' softmax ping-pong against the tensor core.
+//              two tiles' softmax ping-pong against the tensor core; P is released
+//              in two parts so each PV starts on the first half of the block.
 // TMEM (512 columns): S0 [0,128) S1 [128,256) (P_t aliases S_t's first 64
 // columns as packed bf16), O0 [256, 256+D), O1 [256+D, 256+2D).
+// Epilogue: O_t is released right after tile t's last PV; each softmax warp
+// converts its 32 rows to bf16 in 32-column chunks through a 64-byte-swizzled
+// smem tile written to global by TMA stores (rows past Q_LEN clipped).
 //
 // The softmax applies score_mod to every live score and mask_mod (with the
 // q<Q_LEN, kv<KV_LEN bounds of bound_mask, block_mask.cpp:14-19) only in

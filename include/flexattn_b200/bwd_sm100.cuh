@@ -70,8 +70,6 @@ struct BwdParams {
   const int32_t* fkv_num;
   const int32_t* fkv_idx;
   int* turn;           // deterministic mode: per (b*Hq + h, q block) count of finished dQ adds
-  int* dq_cnt;         // in-kernel dQ conversion: per (b*Hq + h, q block) count of landed adds
-  __nv_bfloat16* dq_out;  // in-kernel dQ conversion: the bf16 dQ
   const float* lse2;   // (B*Hq, Lq_pad): cterm, see bwd_preprocess_kernel
   const float* delta;  // (B*Hq, Lq_pad)
   float* dq_acc;       // (B*Hq, Lq, D) fp32
@@ -122,20 +120,6 @@ constexpr bool kDkSS = FA_BWD_DKSS != 0;
 #ifndef FA_BWD_DQ_TMA
 #define FA_BWD_DQ_TMA 1
 #endif
-#ifndef FA_BWD_INCONV
-#define FA_BWD_INCONV 0  // 1: dQ fp32 -> bf16 inside the main kernel (warps 14-15, last contributor);
-                         // measured: free when the conversion is skipped (C2 -3..4 %), but the two
-                         // converter warps (L2-latency-bound, ~64 KB per 6000 cycles) fall behind the
-                         // last contributor's block rate and their queue stalls the dQ drain
-                         // (C3 +12 %, C4 +26 %): off
-#endif
-#ifndef FA_BWD_CONV_LAG
-#define FA_BWD_CONV_LAG 3  // blocks between a dQ block's reduce-adds and their completion wait
-#endif
-#ifndef FA_BWD_CONV_RELAXED
-#define FA_BWD_CONV_RELAXED 1  // the conversion count: 1 relaxed atomic, 2 proxy fence + relaxed, 0 acq_rel
-#endif
-constexpr int kConvSlots = 8;
 template <int D>
 struct BCfg {
   static constexpr int kChunks = D / 64;
@@ -166,10 +150,6 @@ struct alignas(1024) BSmem {
   uint64_t item_full[2], item_empty[2];
   int32_t uitem[2];
   uint32_t tmem_base;
-  // in-kernel dQ conversion: jobs (b*Hq + h, q block) from the reduction warps to warps 14-15
-  int32_t conv_job[kConvSlots];
-  int32_t conv_tail;
-  uint64_t conv_full[kConvSlots], conv_empty[kConvSlots];
 };
 
 struct KvItem {
@@ -303,9 +283,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = BCfg<D>;
   constexpr bool kDet = kMode == kModeDet;
   constexpr bool kNoDQ = kMode == kModeNoDQ;
-  // dQ converted to bf16 in this kernel: the reduction warp whose count completes a q block
-  // (4 warps x the kv blocks in its row's list) hands it to warps 14-15
-  constexpr bool kConv = FA_BWD_INCONV != 0 && kMode == kModeFused && C::kTmaReduce;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   BSmem<D>& sm = *reinterpret_cast<BSmem<D>*>(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -327,11 +304,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.do_full[s], 1);
       mbar_init(&sm.do_free[s], 1);  // the dV MMA commit
     }
-    for (int s = 0; s < kConvSlots; ++s) {
-      mbar_init(&sm.conv_full[s], 1);
-      mbar_init(&sm.conv_empty[s], 2);  // both converter warps
-    }
-    sm.conv_tail = 0;
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.p_full, 8);
     mbar_init(&sm.dp_full, 1);
@@ -810,51 +782,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wq = warp & 3;
     const uint32_t tm = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     int blk = 0, stage_it = 0;
-    // in-kernel conversion: this warp's last kConvLag blocks, each counted once its adds have
-    // landed (waiting on the newest block's writes would stall the dQ drain)
-    constexpr int kConvLag = FA_BWD_CONV_LAG;
-    int pend[kConvLag], pend_target[kConvLag];
-#pragma unroll
-    for (int i = 0; i < kConvLag; ++i) pend[i] = -1, pend_target[i] = 0;
-    auto conv_push = [&](int job) {  // one thread
-      const int k = atomicAdd(&sm.conv_tail, 1);
-      const int s = k % kConvSlots;
-      mbar_wait(&sm.conv_empty[s], ((k / kConvSlots) & 1) ^ 1);
-      sm.conv_job[s] = job;
-      mbar_arrive(&sm.conv_full[s]);
-    };
-    auto conv_settle = [&](int job, int target) {  // lane 0: job's reduce-adds are complete
-      if (job >= 0) {
-        int old;
-        if constexpr (FA_BWD_CONV_RELAXED == 1) {
-          // the adds are complete (bulk_wait_group): performed in L2, where the converter's
-          // L2-only loads read; a gpu-scope release here would also wait for the adds still
-          // in flight (the newer blocks') and stall the drain
-          asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.dq_cnt + job) : "memory");
-        } else if constexpr (FA_BWD_CONV_RELAXED == 2) {
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.dq_cnt + job) : "memory");
-        } else {
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.dq_cnt + job) : "memory");
-        }
-        if (old == target - 1) conv_push(job);
-      }
-    };
-    auto conv_block_done = [&](int b, int h, int r) {  // after this block's reduce-adds were issued
-      if (lane == 0) {
-        // groups older than the last kConvLag blocks (kRed per block) are complete
-        constexpr int kRed = D == 128 ? 4 : 1;
-        bulk_wait_group<kRed * kConvLag>();
-        conv_settle(pend[0], pend_target[0]);
-#pragma unroll
-        for (int i = 0; i + 1 < kConvLag; ++i) pend[i] = pend[i + 1], pend_target[i] = pend_target[i + 1];
-        const int mb = p.bm_b == 1 ? 0 : b, mh = p.bm_h == 1 ? 0 : h;
-        const long long slot = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r;
-        pend[kConvLag - 1] = (b * p.Hq + h) * p.rows + r;
-        pend_target[kConvLag - 1] = 4 * (__ldg(p.kv_num + slot) + __ldg(p.fkv_num + slot));
-      }
-    };
     for (int n = 0;; ++n) {
       const int buf = n & 1;
       mbar_wait(&sm.item_full[buf], (n >> 1) & 1);
@@ -907,7 +834,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (turn != nullptr) det_finish_turn(turn, lane);
-            if constexpr (kConv) conv_block_done(b, h, r);
           } else {
           // per q row the warp's 32 lanes add 32 consecutive floats: one 128-byte line per red
           const int d = wq * 32 + lane;
@@ -955,7 +881,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               bulk_commit_group();
             }
             if (turn != nullptr) det_finish_turn(turn, lane);
-            if constexpr (kConv) conv_block_done(b, h, r);
             ++stage_it;
           } else {
             const int qrow = r * kTile + wq * 32 + lane;
@@ -1009,52 +934,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&sm.dkdv_free);
     }
     if constexpr (C::kTmaReduce && !kNoDQ) {
-      if (lane == 0) {
-        bulk_wait_group<0>();  // every dQ reduce-add has landed before exit
-        if constexpr (kConv) {
-#pragma unroll
-          for (int i = 0; i < kConvLag; ++i) conv_settle(pend[i], pend_target[i]);
-        }
-      }
+      if (lane == 0) bulk_wait_group<0>();  // every dQ reduce-add has landed before exit
       __syncwarp();
-    }
-    if constexpr (kConv) {
-      named_bar_sync(1, 128);  // the four reduction warps have queued all their jobs
-      if (warp == 8 && lane == 0) conv_push(-1);
-    }
-    FA_BWD_TEARDOWN();
-  } else if (kConv) {
-    // ===================== dQ conversion (warps 14-15) =====================
-    // A q block whose adds have all landed in the fp32 accumulator (L2-resident: its kv blocks
-    // were just processed) becomes bf16 dQ: 64 threads, 16-byte L2 loads, 8 in flight each.
-    const int ct = threadIdx.x - 448;
-    for (int k = 0;; ++k) {
-      const int s = k % kConvSlots;
-      mbar_wait(&sm.conv_full[s], (k / kConvSlots) & 1);
-      const int job = *reinterpret_cast<volatile int32_t*>(&sm.conv_job[s]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.conv_empty[s]);
-      if (job < 0) break;
-      __threadfence();
-      const int r = job % p.rows, bh = job / p.rows;
-      const int nq = min(kTile, p.Lq - r * kTile);
-      const long long base = (static_cast<long long>(bh) * p.Lq + r * kTile) * D;
-      const float4* src = reinterpret_cast<const float4*>(p.dq_acc + base);
-      uint2* dst = reinterpret_cast<uint2*>(p.dq_out + base);
-      const int n4 = nq * D / 4;
-      for (int i0 = 0; i0 < n4; i0 += 64 * 8) {
-        float4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = i0 + u * 64 + ct;
-          if (i < n4) v[u] = __ldcg(src + i);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = i0 + u * 64 + ct;
-          if (i < n4) dst[i] = make_uint2(pack_bf16(v[u].x, v[u].y), pack_bf16(v[u].z, v[u].w));
-        }
-      }
     }
     FA_BWD_TEARDOWN();
   } else {
@@ -1072,8 +953,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad, int D, float scale, ScoreT score,
     float* __restrict__ cterm, float* __restrict__ delta, float* __restrict__ dq_acc,
-    int* __restrict__ turn, int* __restrict__ dout_bad, const int32_t* __restrict__ kvn,
-    const int32_t* __restrict__ fkvn, int bm_b, int bm_h, __nv_bfloat16* __restrict__ dq_zero) {
+    int* __restrict__ turn, int* __restrict__ dout_bad) {
   // 8 lanes per row: each lane reads D/8 contiguous bf16 of O and dO with 16-byte loads and
   // zeroes its D/8 floats of the dQ accumulator (the memset of the fp32 workspace, fused)
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
@@ -1090,15 +970,6 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     return;
   }
   const long long src = (bh * Lq + q) * D + sub * (D / 8);
-  if (dq_zero != nullptr) {
-    // in-kernel dQ conversion: q blocks no kv block visits are never converted; their dQ is 0
-    const int b = (int)(bh / Hq), h = (int)(bh % Hq);
-    const long long slot = ((long long)(bm_b == 1 ? 0 : b) * bm_h + (bm_h == 1 ? 0 : h)) * (Lq_pad / kTile) + q / kTile;
-    if (__ldg(kvn + slot) + __ldg(fkvn + slot) == 0) {
-      uint4* z = reinterpret_cast<uint4*>(dq_zero + src);
-      for (int v = 0; v < D / 64; ++v) z[v] = make_uint4(0, 0, 0, 0);
-    }
-  }
   const uint4* o4 = reinterpret_cast<const uint4*>(o + src);
   const uint4* d4 = reinterpret_cast<const uint4*>(dout + src);
   float4* z4 = reinterpret_cast<float4*>(dq_acc + src);
@@ -1162,16 +1033,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
   constexpr bool kDet = kMode == kModeDet, kNoDQ = kMode == kModeNoDQ;
-  constexpr bool kConv = FA_BWD_INCONV != 0 && kMode == kModeFused && BCfg<D>::kTmaReduce;
-  // per (b*Hq + h, q block) counters: the deterministic order's turns or the conversion counts
-  int* turn = (kDet || kConv) ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
+  int* turn = kDet ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
   if (kNoDQ) dq_acc = nullptr;  // dQ comes from its own pass: nothing to zero or convert
   if (opt.events[0]) FA_CHECK_CUDA(cudaEventRecord(opt.events[0], st));
   // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
   bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
-      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc, turn, opt.dout_nonfinite,
-      bm.kv_num, bm.full_num, g.bm_b, g.bm_h, kConv ? static_cast<__nv_bfloat16*>(dq) : nullptr);
+      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc, turn, opt.dout_nonfinite);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
@@ -1189,9 +1057,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.bm_b = g.bm_b; p.bm_h = g.bm_h; p.rows = g.rows; p.cols = g.cols;
   p.q_num = bmt.kv_num; p.q_idx = bmt.kv_idx; p.fq_num = bmt.full_num; p.fq_idx = bmt.full_idx;
   p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.fkv_num = bm.full_num; p.fkv_idx = bm.full_idx;
-  p.turn = kDet ? turn : nullptr;
-  p.dq_cnt = kConv ? turn : nullptr;
-  p.dq_out = static_cast<__nv_bfloat16*>(dq);
+  p.turn = turn;
   p.lse2 = lse2; p.delta = delta; p.dq_acc = dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(dk);
   p.dv = static_cast<__nv_bfloat16*>(dv);
@@ -1267,10 +1133,6 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
     // the dQ pass: dQ accumulated in TMEM per q tile, written as bf16
     const fa_status s = bdq::run<D>(g, q, k, v, dout, lse, delta, dq, bm, mask, score, st);
     if (s != FA_OK) return s;
-    if (opt.events[3]) FA_CHECK_CUDA(cudaEventRecord(opt.events[3], st));
-    return FA_OK;
-  }
-  if constexpr (kConv) {  // dQ already converted by the main kernel
     if (opt.events[3]) FA_CHECK_CUDA(cudaEventRecord(opt.events[3], st));
     return FA_OK;
   }

@@ -58,40 +58,17 @@ namespace {  // internal linkage: every including translation unit has its own c
 #ifndef FA_FWD_EMU_EVERY
 #define FA_FWD_EMU_EVERY 4  // one exponential pair in this many is emulated
 #endif
-#ifndef FA_FWD_EMU_NOSPLIT
-#define FA_FWD_EMU_NOSPLIT 0  // 1: the same FMA-pipe share for the unsplit (unit-gradient) scores
-#endif
-#ifndef FA_FWD_ALIBI_TAB
-#define FA_FWD_ALIBI_TAB 0  // 1: ALiBi column term slope*log2e*i from a per-item smem table
-#endif
 #ifndef FA_FWD_ALIBI_REG
 #define FA_FWD_ALIBI_REG 1  // ALiBi column term of a 32-column chunk in registers (float2 pairs): +5 % C2
-#endif
-#ifndef FA_FWD_FUSED
-#define FA_FWD_FUSED 0  // 1: stale-max single pass (max and exponentials together) after a row's first block (-7 % C2/C3, off)
-#endif
-#ifndef FA_FWD_WARP_ARRIVE
-#define FA_FWD_WARP_ARRIVE 0  // 1: P release by one arrival per warp (after __syncwarp) instead of per thread
-#endif
-#ifndef FA_FWD_OSTAGE
-#define FA_FWD_OSTAGE 2  // epilogue O through a per-warp smem tile: 1 coalesced st.global, 2 TMA store
 #endif
 #ifndef FA_FWD_EARLY_O
 #define FA_FWD_EARLY_O 1  // O_t released to the epilogue right after tile t's last PV
 #endif
-#ifndef FA_FWD_LISTWARP
-#define FA_FWD_LISTWARP 1  // warp 10 builds the item lists (warp-parallel) while warp 8 loads Q
-#endif
-#ifndef FA_FWD_SPLITP
-#define FA_FWD_SPLITP 1  // every score variant releases P in parts (C2 +1.4 %, C3 +2.2 %)
-#endif
 #ifndef FA_FWD_PPARTS
-#define FA_FWD_PPARTS 2  // parts of P released separately (2 or 4)
+#define FA_FWD_PPARTS 2  // parts of P released separately (2 or 4; 4 measured -3 %)
 #endif
 constexpr int kPParts = FA_FWD_PPARTS;
-template <class ScoreT>
-constexpr bool split_p() { return FA_FWD_SPLITP != 0 || !ScoreT::kUnitGrad; }
-constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, 2 idle) warpgroup
+constexpr int kThreads = 384;  // 2 softmax warpgroups + (producer, MMA, list builder, idle) warpgroup
 constexpr int kTile = 128;           // query rows per tile == kv rows per block
 constexpr int kMaxCols = 1024;       // max kv blocks per row (KV_LEN <= 131072)
 constexpr float kLog2e = 1.4426950408889634f;
@@ -141,10 +118,9 @@ struct alignas(1024) Smem {
   uint8_t k[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   uint8_t v[Cfg<D>::kStages][Cfg<D>::kTileBytes];
   int32_t ulist[2][kMaxCols];
-  uint32_t ubits[4][kMaxCols / 32];  // FA_FWD_LISTWARP: the list builder's column bitmaps
-  int32_t claim_item[2];             // FA_FWD_LISTWARP: item handed to the list builder
+  uint32_t ubits[4][kMaxCols / 32];  // the list builder's column bitmaps
+  int32_t claim_item[2];             // item handed to the list builder
   uint64_t claim_full[2];
-  float coltab[2][2][kTile];  // [tile][item parity][kv]: ALiBi column term (FA_FWD_ALIBI_TAB)
   alignas(512) uint8_t ostage[8][32 * 64];  // epilogue: per softmax warp, 32 rows x 32 bf16 (64-byte swizzle)
   int32_t ulen[2];
   int32_t uitem[2];   // work item of the buffer, -1 = no more work
@@ -192,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.s_full[t], 1);
       // split P (soft-capped scores): one arrival per warp and half; else per thread, [1] only
       for (int pp = 0; pp < kPParts; ++pp)
-        mbar_init(&sm.p_full[t][pp], (split_p<ScoreT>() || FA_FWD_WARP_ARRIVE != 0) ? 4 : 128);
+        mbar_init(&sm.p_full[t][pp], 4);  // one arrival per softmax warp
       mbar_init(&sm.o_full[t], 1);
       mbar_init(&sm.item_full[t], 1);
       mbar_init(&sm.item_empty[t], 1 + 8);
@@ -234,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } while (0)
   if (warp >= 8) {
     reg_dealloc<56>();
-    if (FA_FWD_LISTWARP != 0 && warp == 8 && lane == 0) {
+    if (warp == 8 && lane == 0) {
       // ===================== TMA producer (lists built by warp 10) =====================
       // claims an item, hands it to the list builder, loads its Q tiles while the list is
       // being built, then streams the K/V blocks of the list
@@ -280,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         item = static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
       }
-    } else if (FA_FWD_LISTWARP != 0 && warp == 10) {
+    } else if (warp == 10) {
       // ===================== list builder =====================
       // the union of the item's two rows' visit lists in descending block order (blocks nearest
       // the diagonal first, so the running max is established early): one bitmap word of 32
@@ -352,82 +328,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           ftrace(p, n, 19);
         }
       }
-    } else if (FA_FWD_LISTWARP == 0 && warp == 8 && lane == 0) {
-      // ===================== TMA producer =====================
-      int kv_it = 0;
-      for (int n = 0;; ++n) {
-        const int item = n == 0 ? static_cast<int>(blockIdx.x)
-                                : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
-        const int buf = n & 1;
-        mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
-        if (item >= p.num_items) {
-          sm.uitem[buf] = -1;
-          mbar_arrive(&sm.item_full[buf]);
-          break;
-        }
-        const Item it = decode_item(p, item);
-        sm.uitem[buf] = item;
-        // ---- union of the two rows' visit lists (ascending merge) ----
-        const int mb = p.bm_b == 1 ? 0 : it.b, mh = p.bm_h == 1 ? 0 : it.h;
-        const int r0 = 2 * it.pair, r1 = r0 + 1;
-        const long long s0 = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r0;
-        const int np0 = __ldg(p.kv_num + s0), nf0 = __ldg(p.full_num + s0);
-        const int np1 = r1 < p.rows ? __ldg(p.kv_num + s0 + 1) : 0;
-        const int nf1 = r1 < p.rows ? __ldg(p.full_num + s0 + 1) : 0;
-        const int32_t* pi0 = p.kv_idx + s0 * p.cols;
-        const int32_t* fi0 = p.full_idx + s0 * p.cols;
-        const int32_t* pi1 = pi0 + p.cols;
-        const int32_t* fi1 = fi0 + p.cols;
-        // descending merge: blocks nearest the diagonal first, so the running max is
-        // established early and lazy rescaling of O almost never triggers (ALiBi, causal)
-        int a = np0 - 1, bq = nf0 - 1, c = np1 - 1, d = nf1 - 1, len = 0;
-        int va = a >= 0 ? __ldg(pi0 + a) : -1;
-        int vb = bq >= 0 ? __ldg(fi0 + bq) : -1;
-        int vc = c >= 0 ? __ldg(pi1 + c) : -1;
-        int vd = d >= 0 ? __ldg(fi1 + d) : -1;
-        while (true) {
-          const int col = max(max(va, vb), max(vc, vd));
-          if (col < 0) break;
-          uint32_t e = static_cast<uint32_t>(col);
-          if (va == col) { e |= kIn0; --a; va = a >= 0 ? __ldg(pi0 + a) : -1; }
-          if (vb == col) { e |= kIn0 | kFull0; --bq; vb = bq >= 0 ? __ldg(fi0 + bq) : -1; }
-          if (vc == col) { e |= kIn1; --c; vc = c >= 0 ? __ldg(pi1 + c) : -1; }
-          if (vd == col) { e |= kIn1 | kFull1; --d; vd = d >= 0 ? __ldg(fi1 + d) : -1; }
-          sm.ulist[buf][len++] = static_cast<int32_t>(e);
-        }
-        sm.ulen[buf] = len;
-        mbar_arrive(&sm.item_full[buf]);
-        ftrace(p, n, 19);
-        // ---- Q tiles ----
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&sm.q_free[t], (n & 1) ^ 1);
-          mbar_expect_tx(&sm.q_full[t], C::kTileBytes);
-          for (int ch = 0; ch < C::kChunks; ++ch)
-            tma_load_3d(sm.q[t] + ch * C::kChunkBytes, &tmQ, &sm.q_full[t], ch * 64,
-                        (r0 + t) * kTile, it.b * p.Hq + it.h);
-        }
-        ftrace(p, n, 20);
-        // ---- K/V blocks ----
-        const int kb = p.Bkv == 1 ? 0 : it.b, kh = it.h / p.G;
-        for (int j = 0; j < len; ++j, ++kv_it) {
-          const int st = kv_it % C::kStages;
-          // K_j's slot frees when the QKs of block j-2 complete (an iteration before V's)
-          const int colb = static_cast<int>(static_cast<uint32_t>(sm.ulist[buf][j]) & kColMask);
-          mbar_wait(&sm.k_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
-          ftrace(p, kv_it, 12);
-          if (j == 0) ftrace(p, n, 26);
-          mbar_expect_tx(&sm.k_full[st], C::kTileBytes);
-          for (int ch = 0; ch < C::kChunks; ++ch)
-            tma_load_3d(sm.k[st] + ch * C::kChunkBytes, &tmK, &sm.k_full[st], ch * 64,
-                        colb * kTile, kb * p.Hkv + kh);
-          mbar_wait(&sm.v_empty[st], ((kv_it / C::kStages) & 1) ^ 1);
-          ftrace(p, kv_it, 13);
-          mbar_expect_tx(&sm.v_full[st], C::kTileBytes);
-          for (int ch = 0; ch < C::kChunks; ++ch)
-            tma_load_3d(sm.v[st] + ch * C::kChunkBytes, &tmV, &sm.v_full[st], ch * 64,
-                        colb * kTile, kb * p.Hkv + kh);
-        }
-      }
     } else if (warp == 9) {
       // ===================== MMA issuer =====================
       // The whole warp runs the (warp-uniform) control flow and one elected lane issues:
@@ -462,29 +362,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // O_t += P_t V: each part of the kv block (128 / kPParts kv, P columns of that part) as
       // soon as the softmax released it
-      constexpr bool kSplitP = split_p<ScoreT>();  // see the softmax
       auto issue_pv = [&](int t, int st, bool acc, uint32_t ph) {
         const uint64_t b0 = make_sdesc_sw128(smem_u32(sm.v[st]), C::kChunkBytes, 1024);
-        if constexpr (kSplitP) {
-          constexpr int kSteps = (kTile / 16) / kPParts;
+        constexpr int kSteps = (kTile / 16) / kPParts;
 #pragma unroll
-          for (int hf = 0; hf < kPParts; ++hf) {
-            mbar_wait(&sm.p_full[t][hf], ph);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-              for (int kk = hf * kSteps; kk < hf * kSteps + kSteps; ++kk)
-                umma_ts(tm + 256 + t * D, tm + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
-                        (acc || kk > 0) ? 1u : 0u);
-            }
-            __syncwarp();
-          }
-        } else {
-          mbar_wait(&sm.p_full[t][1], ph);
+        for (int hf = 0; hf < kPParts; ++hf) {
+          mbar_wait(&sm.p_full[t][hf], ph);
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < kTile / 16; ++kk)
+            for (int kk = hf * kSteps; kk < hf * kSteps + kSteps; ++kk)
               umma_ts(tm + 256 + t * D, tm + t * 128 + kk * 8, b0 + kk * (2048 >> 4), idesc_pv,
                       (acc || kk > 0) ? 1u : 0u);
           }
@@ -590,15 +477,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item it = decode_item(p, item);
       const int len = sm.ulen[buf];
       const int qi = (2 * it.pair + t) * kTile + row;
-      // ALiBi: the column part of the bias, -slope·log2e·i for kv = kv0 + i, is the same for
-      // every row and block of the item: one smem table per item (double-buffered by item
-      // parity; the tile's warps are never two items apart) read with broadcast LDS.128
-      constexpr bool kAlibiTab = FA_FWD_ALIBI_TAB != 0 && ScoreT::kKind == 1;
-      const float* ctab = sm.coltab[t][n & 1];
-      if constexpr (kAlibiTab) {
-        sm.coltab[t][n & 1][row] = -__ldg(score.p.slopes + it.h) * kLog2e * static_cast<float>(row);
-        named_bar_sync(1 + t, 128);
-      }
       // ALiBi in registers: the column term step·i of a 32-column chunk as 16 float2 pairs (per
       // item: the slope is the head's); the chunk's offset (row term + step·32·chunk) joins the
       // max and the exponent per chunk, so a pair of scores costs one FFMA2
@@ -648,12 +526,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), abias[(i & 31) >> 1]);
             v0 = vv.x;
             v1 = vv.y;
-          } else if constexpr (kAlibiTab) {
-            // s·c + column term; the row term (rowc.base) joins the max and the exponent
-            const float2 ct = *reinterpret_cast<const float2*>(ctab + i);
-            const float2 vv = __ffma2_rn(make_float2(v0, v1), make_float2(rowc.c, rowc.c), ct);
-            v0 = vv.x;
-            v1 = vv.y;
           } else if constexpr (!kPlain) {
             const auto rc = rowc.shifted(i & ~31);
             v0 = rc.log2(v0, i & 31);
@@ -682,71 +554,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           float mx = fmaxf(fmaxf(acc[0], acc[1]), fmaxf(acc[2], acc[3]));
           if constexpr (kPlain) mx *= rowc.c;
-          if constexpr (kAlibiTab) mx += rowc.base;  // -inf stays -inf
           return mx;
         };
-        constexpr bool kSplitP = split_p<ScoreT>();
         const float2 xs2 = make_float2(kPlain ? rowc.c : 1.f, kPlain ? rowc.c : 1.f);
-        // Stale-max single pass (every block but a row's first): the exponentials use the
-        // running max m while the block max is still being accumulated, so the MUFU work starts
-        // right after the TMEM load instead of after a separate max pass. If the block raised a
-        // row's max past the lazy-rescale threshold (or the row had no max yet) the warp
-        // discards the pass and runs the two-pass path below; otherwise the result is exactly
-        // what the two-pass path computes (it keeps the stale max too).
-        constexpr bool kFused = FA_FWD_FUSED != 0 && !kSplitP && !kAlibiTab;
-        if constexpr (kFused) {
-          if (__any_sync(0xffffffffu, m != -INFINITY)) {
-            const float msub0 = (m == -INFINITY) ? 0.f : m;
-            float2 nmc[4];
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) nmc[cc] = make_float2(coff[cc] - msub0, coff[cc] - msub0);
-            float fm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            float2 fl[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                            make_float2(0.f, 0.f)};
-            uint32_t pk[64];
-            auto fpass = [&](auto masked) {
-#pragma unroll
-              for (int i = 0; i < 128; i += 2) {
-                float v0, v1;
-                score_pair(i, masked, v0, v1);
-                max_acc(fm4, i, v0, v1);
-                const float2 x = __ffma2_rn(make_float2(v0, v1), xs2, nmc[i >> 5]);
-                const float2 pv = make_float2(ex2(x.x), ex2(x.y));
-                fl[(i >> 1) & 3] = __fadd2_rn(fl[(i >> 1) & 3], pv);
-                pk[i >> 1] = pack_bf16(pv.x, pv.y);
-              }
-            };
-            if (full) fpass(std::false_type{});
-            else fpass(std::true_type{});
-            const float fmx = block_max(fm4);
-            const float fm_new = fmaxf(m, fmx);
-            const bool redo = (m == -INFINITY) ? (fm_new != -INFINITY) : (fm_new > m + kRescaleThreshold);
-            if (!__any_sync(0xffffffffu, redo)) {
-              tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-              tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-              tmem_wait_st();
-              tc_fence_before();
-              if constexpr (FA_FWD_WARP_ARRIVE != 0) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.p_full[t][1]);
-              } else {
-                mbar_arrive(&sm.p_full[t][1]);
-              }
-              const float2 l01 = __fadd2_rn(fl[0], fl[1]), l23 = __fadd2_rn(fl[2], fl[3]);
-              const float2 lt = __fadd2_rn(l01, l23);
-              l += lt.x + lt.y;
-              if (row == 0) ftrace(p, gs, t * 2 + 1);
-              ++gs;
-              continue;  // (not a flag: r must be dead on this path for the register allocator)
-            } else {
-              // the scores are still in TMEM (P has not been written): reload them
-#pragma unroll
-              for (int cc = 0; cc < 4; ++cc)
-                tmem_ld32(s_tm + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[cc * 32]));
-              tmem_wait_ld();
-            }
-          }
-        }
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         auto pass1 = [&](auto masked) {
 #pragma unroll
@@ -789,11 +599,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // masked score), chosen by column alone, so a block gives the same P whether it is
         // classified full or partial (demote_full_to_partial / promote stay bit-exact).
         float nmv = -msub;
-        if constexpr (kAlibiTab) nmv = rowc.base - msub;  // the ALiBi row term rejoins here
         const float2 nm2 = make_float2(nmv, nmv);
         float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
-        if constexpr (kSplitP) {
+        {
           constexpr int kPairs = 64 / kPParts;  // packed P columns per part
           auto exp_part = [&](int hf) {
             uint32_t pk[kPairs];
@@ -820,35 +629,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           };
 #pragma unroll
           for (int hf = 0; hf < kPParts; ++hf) exp_part(hf);
-        } else {
-          uint32_t pk[64];
-          auto exp_all = [&](auto emulate) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              float2 nmc = nm2;
-              if constexpr (kAlibiReg) nmc = make_float2(nm2.x + coff[i >> 4], nm2.y + coff[i >> 4]);
-              const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
-                                          xs2, nmc);
-              float2 pv;
-              if (decltype(emulate)::value && (i % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
-                pv = exp2_poly2(x);
-              else pv = make_float2(ex2(x.x), ex2(x.y));
-              ls[i & 3] = __fadd2_rn(ls[i & 3], pv);
-              pk[i] = pack_bf16(pv.x, pv.y);
-            }
-          };
-          if (FA_FWD_EMU_NOSPLIT != 0 && full) exp_all(std::true_type{});
-          else exp_all(std::false_type{});
-          tmem_st32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-          tmem_st32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-          tmem_wait_st();
-          tc_fence_before();
-          if constexpr (FA_FWD_WARP_ARRIVE != 0) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.p_full[t][1]);
-          } else {
-            mbar_arrive(&sm.p_full[t][1]);
-          }
         }
         const float2 l01 = __fadd2_rn(ls[0], ls[1]), l23 = __fadd2_rn(ls[2], ls[3]);
         const float2 lt = __fadd2_rn(l01, l23);
@@ -864,24 +644,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = qi < p.Lq;
       const long long slot = (static_cast<long long>(it.b) * p.Hq + it.h) * p.Lq + qi;
       __nv_bfloat16* orow = p.out + slot * D;
-      if (FA_FWD_OSTAGE != 0 && any_blocks) {
-        // 32 columns at a time through a per-warp smem tile, stored as 8 rows x 64 contiguous
-        // bytes per instruction (a row-per-thread store touches 32 lines per instruction and
-        // kept the LSU busy for ~5000 cycles at every item boundary)
+      if (any_blocks) {
+        // 32 columns at a time through a per-warp 64-byte-swizzled smem tile and one TMA store of
+        // 32 rows x 32 columns (row-per-thread global stores touch 32 lines per instruction and
+        // kept the LSU busy ~5000 cycles at every item boundary)
         const float inv = l > 0.f ? 1.f / l : 0.f;
         uint8_t* stg = sm.ostage[warp];
         const int qrow0 = (2 * it.pair + t) * kTile + wq * 32;
-        const long long slot0 = (static_cast<long long>(it.b) * p.Hq + it.h) * p.Lq;
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t r0[32];
           tmem_ld32(o_tm + cc * 32, r0);
           tmem_wait_ld();
           if (row == 0 && t == 0) ftrace(p, n, 27 + cc);
-          if constexpr (FA_FWD_OSTAGE == 2) {  // the previous TMA store has read the tile
-            if (lane == 0) bulk_wait_group_read<0>();
-            __syncwarp();
-          }
+          if (lane == 0) bulk_wait_group_read<0>();  // the previous TMA store has read the tile
+          __syncwarp();
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             uint4 w;
@@ -891,47 +668,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             w.w = pack_bf16(__uint_as_float(r0[8 * k + 6]) * inv, __uint_as_float(r0[8 * k + 7]) * inv);
             *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = w;
           }
-          if constexpr (FA_FWD_OSTAGE == 2) {
-            // the tile is in the SWIZZLE_64B layout: one TMA store of 32 rows x 32 columns
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_3d(&tmO, stg, cc * 32, qrow0, it.b * p.Hq + it.h);
-              bulk_commit_group();
-            }
-            continue;
-          }
+          fence_proxy_async();
           __syncwarp();
-#pragma unroll
-          for (int i8 = 0; i8 < 4; ++i8) {
-            const int rr = i8 * 8 + (lane >> 2), sg = lane & 3;
-            const uint4 w = *reinterpret_cast<const uint4*>(stg + rr * 64 + ((sg ^ ((rr >> 1) & 3)) << 4));
-            if (qrow0 + rr < p.Lq)
-              *reinterpret_cast<uint4*>(p.out + (slot0 + qrow0 + rr) * D + cc * 32 + sg * 8) = w;
-          }
-          __syncwarp();
-        }
-      } else if (any_blocks) {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-        for (int cc = 0; cc < D / 64; ++cc) {
-          uint32_t r0[32], r1[32];
-          tmem_ld32(o_tm + cc * 64, r0);
-          tmem_ld32(o_tm + cc * 64 + 32, r1);
-          tmem_wait_ld();
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + cc * 64);
-#pragma unroll
-            for (int v4 = 0; v4 < 8; ++v4) {
-              const uint32_t* r = v4 < 4 ? r0 : r1;
-              const int o = (v4 & 3) * 8;
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(r[o + 0]) * inv, __uint_as_float(r[o + 1]) * inv);
-              w.y = pack_bf16(__uint_as_float(r[o + 2]) * inv, __uint_as_float(r[o + 3]) * inv);
-              w.z = pack_bf16(__uint_as_float(r[o + 4]) * inv, __uint_as_float(r[o + 5]) * inv);
-              w.w = pack_bf16(__uint_as_float(r[o + 6]) * inv, __uint_as_float(r[o + 7]) * inv);
-              dst[v4] = w;
-            }
+          if (lane == 0) {
+            tma_store_3d(&tmO, stg, cc * 32, qrow0, it.b * p.Hq + it.h);
+            bulk_commit_group();
           }
         }
       } else if (valid) {
@@ -944,10 +685,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.item_empty[buf]);
     }
-    if constexpr (FA_FWD_OSTAGE == 2) {
-      if (lane == 0) bulk_wait_group<0>();  // the epilogue's TMA stores have landed
-      __syncwarp();
-    }
+    if (lane == 0) bulk_wait_group<0>();  // the epilogue's TMA stores have landed
+    __syncwarp();
     FA_FWD_TEARDOWN();
   }
 #undef FA_FWD_TEARDOWN
@@ -960,7 +699,7 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, vo
   CUtensorMap mq, mk, mv, mo{};
   fa_status s;
   if ((s = make_map(&mq, q, g.B * g.Hq, g.Lq, D)) != FA_OK) return s;
-  if (FA_FWD_OSTAGE == 2) {
+  {
     const CUresult r = encode_o32_map(&mo, o, g.B * g.Hq, g.Lq, D);
     FA_REQUIRE(r == CUDA_SUCCESS, FA_CUDA_ERROR,
                "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");

@@ -111,6 +111,9 @@ constexpr bool kDkSS = FA_BWD_DKSS != 0;
 #ifndef FA_BWD_PAIRED
 #define FA_BWD_PAIRED 0  // 1: phase A's exponents of plain / ALiBi scores as FFMA2 pairs
 #endif
+#ifndef FA_BWD_NODQ_DO2
+#define FA_BWD_NODQ_DO2 1  // split mode (no dQ staging): two dO stages
+#endif
 #ifndef FA_BWD_L2PF
 #define FA_BWD_L2PF 0  // 1: L2 prefetch of the next task's Q / dO tiles (one task ahead)
 #endif
@@ -133,19 +136,21 @@ struct BCfg {
   static constexpr int kStageFloats = kTmaReduce ? 32 * kBoxD : 4;
 };
 
-template <int D>
+// kDoSt: dO stages (the split mode's dK/dV kernel has no dQ staging and spends it on a second
+// dO stage)
+template <int D, int kDoSt = BCfg<D>::kDoStages, int kStageFl = BCfg<D>::kStageFloats>
 struct alignas(1024) BSmem {
   uint8_t k[BCfg<D>::kTileBytes];
   uint8_t v[BCfg<D>::kTileBytes];
   uint8_t q[2][BCfg<D>::kTileBytes];
-  uint8_t dO[BCfg<D>::kDoStages][BCfg<D>::kTileBytes];
+  uint8_t dO[kDoSt][BCfg<D>::kTileBytes];
   uint8_t ds[kTile * kTile * 2];  // dS^T [kv][q], SW128, two 64-wide q chunks
   float lse2[2][kTile];
   float delta[2][kTile];  // Δ rides with the q stage (q_full), so dO frees after dV alone
-  float dq_stage[4][2][BCfg<D>::kStageFloats];  // per reduction warp, double-buffered
+  float dq_stage[4][2][kStageFl];  // per reduction warp, double-buffered
   uint64_t k_full, v_full, k_free, v_free;
   uint64_t q_full[2], q_free[2];
-  uint64_t do_full[BCfg<D>::kDoStages], do_free[BCfg<D>::kDoStages];
+  uint64_t do_full[kDoSt], do_free[kDoSt];
   uint64_t s_full, p_full, dp_full, ds_full, ds_free, dq_full, dq_empty, dkdv_full, dkdv_free;
   uint64_t item_full[2], item_empty[2];
   int32_t uitem[2];
@@ -284,7 +289,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kDet = kMode == kModeDet;
   constexpr bool kNoDQ = kMode == kModeNoDQ;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  BSmem<D>& sm = *reinterpret_cast<BSmem<D>*>(smem_raw);
+  // the split mode keeps no dQ staging and gives its 32 KB to a second dO stage
+  constexpr int kDoSt = (kNoDQ && FA_BWD_NODQ_DO2 != 0) ? 2 : C::kDoStages;
+  using Sm = BSmem<D, kDoSt, (kNoDQ && FA_BWD_NODQ_DO2 != 0) ? 4 : C::kStageFloats>;
+  Sm& sm = *reinterpret_cast<Sm*>(smem_raw);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();  // SWIZZLE_128B operands need 1 KiB alignment
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.item_full[s], 1);
       mbar_init(&sm.item_empty[s], 1 + 8 + 4);
     }
-    for (int s = 0; s < C::kDoStages; ++s) {
+    for (int s = 0; s < kDoSt; ++s) {
       mbar_init(&sm.do_full[s], 1);
       mbar_init(&sm.do_free[s], 1);  // the dV MMA commit
     }
@@ -409,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                           it.kb * p.Hkv + it.kh);
             v_loaded = true;
           }
-          const int ds_ = blk % C::kDoStages;
-          mbar_wait(&sm.do_free[ds_], ((blk / C::kDoStages) & 1) ^ 1);
+          const int ds_ = blk % kDoSt;
+          mbar_wait(&sm.do_free[ds_], ((blk / kDoSt) & 1) ^ 1);
           trace_ev(p, blk, 11);
           mbar_expect_tx(&sm.do_full[ds_], C::kTileBytes);
           for (int ch = 0; ch < C::kChunks; ++ch)
@@ -465,9 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace_ev(p, b, 4);
       };
       auto issue_dp = [&](int b) {  // dP^T(b) = V dO(b)^T, after dQ(b-1) left TMEM
-        const int ds_ = b % C::kDoStages;
+        const int ds_ = b % kDoSt;
         trace_ev(p, b, 14);
-        mbar_wait(&sm.do_full[ds_], (b / C::kDoStages) & 1);
+        mbar_wait(&sm.do_full[ds_], (b / kDoSt) & 1);
         trace_ev(p, b, 15);
         if constexpr (!kNoDQ) mbar_wait(&sm.dq_empty, (b & 1) ^ 1);  // dQ^T(b-1) left TMEM
         trace_ev(p, b, 16);
@@ -476,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         trace_ev(p, b, 6);
       };
       auto issue_dv = [&](int b, bool acc) {  // dV += P^T(b) dO(b)   (TS)
-        const int ds_ = b % C::kDoStages;
+        const int ds_ = b % kDoSt;
         trace_ev(p, b, 17);
         mbar_wait(&sm.p_full, b & 1);
         trace_ev(p, b, 18);
@@ -1072,7 +1080,8 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
     FA_CHECK_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * kTraceTasks * kTraceEv, st));
   }
   p.trace = trace;
-  const size_t smem = sizeof(BSmem<D>);
+  constexpr bool kNoDQ2 = kMode == kModeNoDQ && FA_BWD_NODQ_DO2 != 0;
+  const size_t smem = sizeof(BSmem<D, kNoDQ2 ? 2 : BCfg<D>::kDoStages, kNoDQ2 ? 4 : BCfg<D>::kStageFloats>);
   auto kern = flex_bwd_sm100_kernel<D, MaskT, ScoreT, kMode>;
   FA_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = p.num_items < num_sms() ? p.num_items : num_sms();

@@ -53,11 +53,16 @@ namespace fwd {
 namespace {  // internal linkage: every including translation unit has its own copy
 
 #ifndef FA_FWD_EMU
-#define FA_FWD_EMU 1  // part of the exponentials on the FMA pipe in full blocks
+#define FA_FWD_EMU 1  // part of the exponentials on the FMA pipe
 #endif
 #ifndef FA_FWD_EMU_EVERY
-#define FA_FWD_EMU_EVERY 4  // one exponential pair in this many is emulated
+#define FA_FWD_EMU_EVERY 4  // one exponential pair in this many is emulated (soft-capped scores)
 #endif
+#ifndef FA_FWD_EMU_EVERY_UNIT
+#define FA_FWD_EMU_EVERY_UNIT 8  // the same for the other scores (one MUFU per score: less to offload)
+#endif
+template <class ScoreT>
+constexpr int emu_every() { return ScoreT::kUnitGrad ? FA_FWD_EMU_EVERY_UNIT : FA_FWD_EMU_EVERY; }
 #ifndef FA_FWD_ALIBI_REG
 #define FA_FWD_ALIBI_REG 1  // ALiBi column term of a 32-column chunk in registers (float2 pairs): +5 % C2
 #endif
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // P = exp2(x - m) as packed bf16 over S's first 64 columns (column c: kv 2c, 2c+1).
         // Each part of P releases its PV MMAs on its own (p_full[t][part]) so the tensor core
         // starts on the first kv of the block while the exponentials of the rest run. One
-        // exponential pair in FA_FWD_EMU_EVERY runs on the FMA pipe (exp2_poly2, exactly 0 for a
+        // exponential pair in emu_every() runs on the FMA pipe (exp2_poly2, exactly 0 for a
         // masked score), chosen by column alone, so a block gives the same P whether it is
         // classified full or partial (demote_full_to_partial / promote stay bit-exact).
         float nmv = -msub;
@@ -614,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
                                           xs2, nmc);
               float2 pv;
-              if (FA_FWD_EMU != 0 && (k % FA_FWD_EMU_EVERY) == FA_FWD_EMU_EVERY - 1)
+              if (FA_FWD_EMU != 0 && (k % emu_every<ScoreT>()) == emu_every<ScoreT>() - 1)
                 pv = exp2_poly2(x);
               else pv = make_float2(ex2(x.x), ex2(x.y));
               ls[k & 3] = __fadd2_rn(ls[k & 3], pv);

@@ -13,9 +13,11 @@ LIBS = [os.path.join(ROOT, "paper_2412_05496_b200", "libflexattn_b200.so"),
         os.path.join(ROOT, "tests", "cpp", "libcustom_mods.so")]
 OPS = ["UTCHMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UTMAREDG", "UTMASTG", "UBLKCP", "MUFU.EX2", "MUFU.TANH",
        "SYNCS.ARRIVE", "SYNCS.PHASECHK"]
-FAMILIES = [("fwd_sm100", "flex_fwd_sm100_kernel"), ("bwd_sm100 (fused)", "flex_bwd_sm100_kernel"),
-            ("bwd_dq (dQ pass)", "flex_bwd_dq_kernel"), ("decode", "decode_kernel"),
-            ("block_mask", "classify_kernel"), ("page_pool", "pool_"), ("fwd_simt", "fwd_simt_kernel")]
+FAMILIES = [("fwd_sm100", "flex_fwd_sm100_kernel"), ("fwd1t (long rows)", "flex_fwd1t_kernel"),
+            ("bwd_sm100 (fused)", "flex_bwd_sm100_kernel"), ("bwd_dq (dQ pass)", "flex_bwd_dq_kernel"),
+            ("bwd_preprocess", "bwd_preprocess_kernel"), ("decode_tc (GQA/multi-row)", "decode_tc_kernel"),
+            ("decode", "decode_kernel"), ("block_mask", "classify_kernel"), ("page_pool", "pool_"),
+            ("fwd_simt", "fwd_simt_kernel"), ("bwd_simt", "bsimt")]
 
 
 def main():

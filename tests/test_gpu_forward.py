@@ -200,3 +200,23 @@ def test_long_rows_take_the_one_tile_kernel(fa, O, dev):
     names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     assert any("flex_fwd1t_kernel" in n for n in names), names
     assert not any("simt" in n for n in names), names
+
+
+@pytest.mark.parametrize("mname", ["noop", "hash:313:60"])
+def test_two_tile_kernel_at_the_widest_rows(fa, O, dev, mname):
+    """1024 kv blocks per row (KV_LEN 131072), the widest the two-tile kernel takes: every lane
+    of the list builder's column bitmap is populated and the union lists hold 1024 entries."""
+    Lq, Lkv = 256, 131072
+    e_o, e_l, _ = run_case(fa, O, dev, mname, "noop", B=1, Hq=1, Hkv=1, Lq=Lq, Lkv=Lkv, D=64)
+    assert e_o <= BF16_TOL and e_l <= BF16_TOL, (e_o, e_l)
+    from torch.profiler import ProfilerActivity, profile
+    fm, _ = mask_pair(mname, Lkv)
+    q = fa.random_tensor(1, (1, 1, Lq, 64), device=dev)
+    kv = fa.random_tensor(2, (1, 1, Lkv, 64), device=dev)
+    bm = fa.create_block_mask(fm, 1, 1, Lq, Lkv, device=dev)
+    assert bm.cols == 1024
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fa.forward(q, kv, kv, fa.noop_score(), bm)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert any("flex_fwd_sm100_kernel" in n for n in names), names

@@ -69,7 +69,6 @@ struct BwdParams {
   const int32_t* kv_idx;
   const int32_t* fkv_num;
   const int32_t* fkv_idx;
-  int* turn;           // deterministic mode: per (b*Hq + h, q block) count of finished dQ adds
   const float* lse2;   // (B*Hq, Lq_pad): cterm, see bwd_preprocess_kernel
   const float* delta;  // (B*Hq, Lq_pad)
   float* dq_acc;       // (B*Hq, Lq, D) fp32
@@ -228,47 +227,9 @@ __device__ __forceinline__ int count_tasks(const BwdParams& p, const KvItem& it)
   return total;
 }
 
-// ---- deterministic dQ (FA_FLAG_DETERMINISTIC) ----
-// The contributions to dQ of q block r of (b, h) come from the kv blocks c of r's kv-side lists,
-// one item each. Each of the 4 reduction warps of the item of rank k (k = number of listed kv
-// blocks < c) waits until all 4 warps of rank k-1 have their TMA reduce-adds complete, so every
-// fp32 element of the accumulator receives its adds in ascending-c order. Waits only point to
-// lower items, and in this mode every item is claimed by a running CTA: no deadlock.
-__device__ __forceinline__ int* det_wait_turn(const BwdParams& p, const KvItem& it, int b, int h, int r,
-                                              int lane) {
-  const int mb = p.bm_b == 1 ? 0 : b, mh = p.bm_h == 1 ? 0 : h;
-  const long long slot = (static_cast<long long>(mb) * p.bm_h + mh) * p.rows + r;
-  const int np = __ldg(p.kv_num + slot), nf = __ldg(p.fkv_num + slot);
-  int rank = 0;
-  for (int i = lane; i < np + nf; i += 32) {
-    const int c = i < np ? __ldg(p.kv_idx + slot * p.cols + i) : __ldg(p.fkv_idx + slot * p.cols + (i - np));
-    rank += __popc(__ballot_sync(__activemask(), c < it.c));
-  }
-  rank = __shfl_sync(0xffffffffu, rank, 0);
-  int* turn = p.turn + static_cast<long long>(b * p.Hq + h) * p.rows + r;
-  if (lane == 0) {
-    const int want = 4 * rank;
-    int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(turn) : "memory");
-    } while (v < want);
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-  __syncwarp();
-  return turn;
-}
-__device__ __forceinline__ void det_finish_turn(int* turn, int lane) {
-  if (lane == 0) {
-    bulk_wait_group<0>();  // this warp's reduce-adds have been performed
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(turn) : "memory");
-  }
-  __syncwarp();
-}
-
-// kMode: kModeFused (dQ reduce-added by the reduction warps), kModeDet (the same with the adds
-// ordered across kv blocks), kModeNoDQ (dK/dV only; dQ by the separate pass in bwd_dq.cuh)
-enum { kModeFused = 0, kModeDet = 1, kModeNoDQ = 2 };
+// kMode: kModeFused (dQ reduce-added by the reduction warps), kModeNoDQ (dK/dV only; dQ by the
+// separate pass in bwd_dq.cuh)
+enum { kModeFused = 0, kModeNoDQ = 2 };
 #ifndef FA_BWD_SPLIT
 #define FA_BWD_SPLIT 0  // 1: the split (dK/dV kernel + dQ pass) backward by default
 #endif
@@ -286,7 +247,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmDQ, const BwdParams p, MaskT mask,
                           ScoreT score) {
   using C = BCfg<D>;
-  constexpr bool kDet = kMode == kModeDet;
   constexpr bool kNoDQ = kMode == kModeNoDQ;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the split mode keeps no dQ staging and gives its 32 KB to a second dO stage
@@ -360,11 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===================== TMA producer =====================
       int blk = 0;
       for (int n = 0;; ++n) {
-        // deterministic mode claims every item from the counter, so an item is only ever
-        // owned by a CTA that is running (the ordered dQ adds wait on lower items only)
-        const int item = kDet ? atomicAdd(p.work_counter, 1)
-                         : n == 0        ? static_cast<int>(blockIdx.x)
-                                         : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
+        const int item = n == 0 ? static_cast<int>(blockIdx.x)
+                                : static_cast<int>(gridDim.x) + atomicAdd(p.work_counter, 1);
         const int buf = n & 1;
         mbar_wait(&sm.item_empty[buf], ((n >> 1) & 1) ^ 1);
         sm.uitem[buf] = item < p.num_items ? item : -1;
@@ -825,8 +782,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (C::kTmaReduce) {
             // four 32 (q) x 32 (d) fp32 tiles per warp: st.shared rows of 128 B (lane = d),
             // then one TMA reduce-add each (rows past Q_LEN are clipped by the tensor map)
-            int* turn = nullptr;
-            if constexpr (kDet) turn = det_wait_turn(p, it, b, h, r, lane);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4, ++stage_it) {
               float* stg = sm.dq_stage[wq][stage_it & 1];
@@ -841,7 +796,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bulk_commit_group();
               }
             }
-            if (turn != nullptr) det_finish_turn(turn, lane);
           } else {
           // per q row the warp's 32 lanes add 32 consecutive floats: one 128-byte line per red
           const int d = wq * 32 + lane;
@@ -868,8 +822,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(&sm.dq_empty);
           if constexpr (C::kTmaReduce) {
             // one 32 (q) x D fp32 tile per warp (row per lane; bank conflicts accepted at D=64)
-            int* turn = nullptr;
-            if constexpr (kDet) turn = det_wait_turn(p, it, b, h, r, lane);
             float* stg = sm.dq_stage[wq][stage_it & 1];
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
@@ -888,7 +840,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_reduce_add_3d(&tmDQ, stg, 0, r * kTile + wq * 32, b * p.Hq + h);
               bulk_commit_group();
             }
-            if (turn != nullptr) det_finish_turn(turn, lane);
             ++stage_it;
           } else {
             const int qrow = r * kTile + wq * 32 + lane;
@@ -961,7 +912,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, int BH, int Hq, int Lq, int Lq_pad, int D, float scale, ScoreT score,
     float* __restrict__ cterm, float* __restrict__ delta, float* __restrict__ dq_acc,
-    int* __restrict__ turn, int* __restrict__ dout_bad) {
+    int* __restrict__ dout_bad) {
   // 8 lanes per row: each lane reads D/8 contiguous bf16 of O and dO with 16-byte loads and
   // zeroes its D/8 floats of the dQ accumulator (the memset of the fp32 workspace, fused)
   const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
@@ -969,7 +920,6 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
   if (row >= (long long)BH * Lq_pad) return;
   const int q = (int)(row % Lq_pad);
   const long long bh = row / Lq_pad;
-  if (turn != nullptr && sub == 0 && (q & (kTile - 1)) == 0) turn[bh * (Lq_pad / kTile) + q / kTile] = 0;
   if (q >= Lq) {
     if (sub == 0) {
       cterm[row] = -INFINITY;
@@ -1040,14 +990,13 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* lse2 = reinterpret_cast<float*>(ws + al(rows * D * 4));
   float* delta = reinterpret_cast<float*>(ws + al(rows * D * 4) + al(prow * 4));
-  constexpr bool kDet = kMode == kModeDet, kNoDQ = kMode == kModeNoDQ;
-  int* turn = kDet ? reinterpret_cast<int*>(ws + al(rows * D * 4) + 2 * al(prow * 4)) : nullptr;
+  constexpr bool kNoDQ = kMode == kModeNoDQ;
   if (kNoDQ) dq_acc = nullptr;  // dQ comes from its own pass: nothing to zero or convert
   if (opt.events[0]) FA_CHECK_CUDA(cudaEventRecord(opt.events[0], st));
   // preprocess: Δ, cterm, and the zeroing of the fp32 dQ accumulator (8 threads per row)
   bwd_preprocess_kernel<ScoreT><<<(unsigned)((prow + 31) / 32), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
-      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc, turn, opt.dout_nonfinite);
+      g.B * g.Hq, g.Hq, g.Lq, Lq_pad, D, g.scale, score, lse2, delta, dq_acc, opt.dout_nonfinite);
   count_launch();
   FA_CHECK_CUDA(cudaGetLastError());
 
@@ -1065,7 +1014,6 @@ fa_status run(const AttnGeom& g, const void* q, const void* k, const void* v, co
   p.bm_b = g.bm_b; p.bm_h = g.bm_h; p.rows = g.rows; p.cols = g.cols;
   p.q_num = bmt.kv_num; p.q_idx = bmt.kv_idx; p.fq_num = bmt.full_num; p.fq_idx = bmt.full_idx;
   p.kv_num = bm.kv_num; p.kv_idx = bm.kv_idx; p.fkv_num = bm.full_num; p.fkv_idx = bm.full_idx;
-  p.turn = turn;
   p.lse2 = lse2; p.delta = delta; p.dq_acc = dq_acc;
   p.dk = static_cast<__nv_bfloat16*>(dk);
   p.dv = static_cast<__nv_bfloat16*>(dv);

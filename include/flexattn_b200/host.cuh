@@ -116,8 +116,8 @@ struct BwdOptions {
 
 // ---- workspace sizes (fa_bwd_workspace_size / fa_decode_workspace_size) ------------------------------
 inline size_t bwd_workspace_bytes(int64_t batch, int64_t heads, int64_t q_len, int64_t dim) {
-  // dq accumulator (fp32) + delta (fp32) + log2-domain lse (fp32) + per-(b, h, q block) turn
-  // counters of the deterministic dQ order, 256-byte aligned pieces
+  // dq accumulator (fp32) + delta (fp32) + log2-domain lse (fp32) + one reserved int per
+  // (b, h, q block) (kept so the size stays ABI-stable), 256-byte aligned pieces
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const size_t rows = static_cast<size_t>(batch * heads * q_len);
   const size_t prow = static_cast<size_t>(batch * heads * ((q_len + 127) / 128 * 128));
